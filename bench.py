@@ -1,0 +1,349 @@
+"""Benchmark: batched CS-WGS holograms/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+Workload (configs[2] with configs[4]'s batching): CS-WGS,
+1152x1152 gaussian pupil (M = 1,042,356), N = 100 random 3D foci
+(x, y ~ U(+-100 um), z ~ U(+-50 um), spot seed 1000+k), compression 1/16,
+I = 20, solver seed k, followed by the e/u quality report.  One step =
+one batch of B independent patterns per GPU (weak scaling: B per rank).
+
+value  : holograms/s over the whole job, inputs resident in HBM, CUDA-event
+         timed per step on the solver stream (L2 flushed between steps).
+e2e    : the same through the C ABI (hs_solve_host) with pinned host
+         buffers: spot + theta0 upload, solve, phase[B][M] float64 +
+         e/u download inside the timed region.
+--impl reference : the CPU oracle (bit-exact restatement of the reference
+         numba kernels, oracle/) on all host threads, one hologram per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "holograms/sec & ms/hologram (1152², N=100, CS-WGS) at 1/2/4/8 B200 vs CPU; e,u"
+SIDE, NSPOTS, COMPRESSION, ITERS = 1152, 100, 1 / 16, 20
+FLOP_PER_PAIR_PASS = 8  # one complex MAC per (pixel, spot) per pass
+
+
+def workload_config(batch):
+    return {"workload": "cswgs_1152_n100_c1/16_i20_batched", "side_px": SIDE,
+            "spots": NSPOTS, "compression": COMPRESSION, "iterations": ITERS,
+            "batch_per_gpu": batch, "pupil": "gaussian waist 6 mm, pitch 9.2 um, "
+            "lambda 800 nm, f 20 mm, seed 0", "foci": "uniform xy +-100 um, z +-50 um, "
+            "spot seed 1000+k, solver seed k", "l2": "flushed between timed steps "
+            "(256 MiB write, outside the step events)"}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def pattern_arrays(first, count):
+    import paper_2003_05293_b200 as hs
+    sets = [hs.random_foci(NSPOTS, 1000 + k) for k in range(first, first + count)]
+    x = np.stack([s.x for s in sets])
+    y = np.stack([s.y for s in sets])
+    z = np.stack([s.z for s in sets])
+    a = np.stack([s.amplitude for s in sets])
+    th = np.stack([np.random.default_rng(k).random(NSPOTS) * 2 * math.pi
+                   for k in range(first, first + count)])
+    return x, y, z, a, th
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index):
+        self.path = tempfile.mktemp(suffix=".csv")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[3:7]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_rate(seconds=10.0, threads=None):
+    """Oracle (bit-exact reference restatement) holograms/s on host cores."""
+    import oracle
+    import paper_2003_05293_b200 as hs
+    pupil = hs.build_pupil(SIDE)
+    threads = threads or oracle.max_threads()
+    done, t0 = 0, time.perf_counter()
+    while True:
+        s = hs.random_foci(NSPOTS, 1000 + done)
+        r = oracle.solve(pupil, s.x, s.y, s.z, s.amplitude, "cswgs", ITERS, COMPRESSION,
+                         seed=done, threads=threads)
+        oracle.quality(pupil, r["tables"], r["phase"], s.amplitude, threads=threads)
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return done / el, done, threads
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    import paper_2003_05293_b200 as hs
+    oracle.build()
+    pupil = hs.build_pupil(SIDE)
+    threads = oracle.max_threads()
+
+    def step(k):
+        s = hs.random_foci(NSPOTS, 1000 + k)
+        r = oracle.solve(pupil, s.x, s.y, s.z, s.amplitude, "cswgs", ITERS, COMPRESSION,
+                         seed=k, threads=threads)
+        return oracle.quality(pupil, r["tables"], r["phase"], s.amplitude, threads=threads)
+
+    for w in range(args.warmup):
+        step(w)
+    t0 = time.perf_counter()
+    eu = [step(args.warmup + k)[:2] for k in range(args.steps)]
+    el = time.perf_counter() - t0
+    val = args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "holograms/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(1),
+            "cpu_baseline": {"value": val, "unit": "holograms/s", "cores": threads,
+                             "kind": "port", "sample": f"{args.steps} holograms of the "
+                             "workload, 1 per step (C+OpenMP oracle, bit-exact vs reference)"},
+            "e2e": {"value": val, "unit": "holograms/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "mean_e": float(np.mean([e for e, _ in eu])),
+            "mean_u": float(np.mean([u for _, u in eu]))}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import paper_2003_05293_b200 as hs
+    from paper_2003_05293_b200 import _lib
+
+    rank, local, world = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist = None
+        torch.cuda.set_device(local)
+    _lib.set_device(local)
+    B = args.batch
+    pupil = hs.build_pupil(SIDE)
+    m = pupil.active_count
+    subset = math.ceil(COMPRESSION * m)
+    plan = _lib.Plan(pupil, local)
+    first = rank * B
+    x, y, z, a, th = pattern_arrays(first, B)
+    plan.set_spot_arrays(x, y, z, a)
+    stream = torch.cuda.ExternalStream(plan.stream(), device=torch.device("cuda", local))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        plan.solve(_lib.ALG_CSWGS, ITERS, subset, th, want_fields=True, sync=True)
+    launches_per_step = plan.last_launch_count()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = Clocks(local)
+    barrier()
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(k))
+            starts[k].record(stream)
+        plan.solve(_lib.ALG_CSWGS, ITERS, subset, th, want_fields=True, sync=False)
+        ends[k].record(stream)
+    barrier()
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    status, _ = plan.status()
+    e, u, _, _, _ = plan.quality_batch()
+    if np.any(status != 0):
+        raise RuntimeError(f"solver failed on patterns {np.nonzero(status)[0]}")
+    if dist is not None:
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * B * args.steps / (total_ms * 1e-3)
+
+    # single-hologram latency (B = 1) on the same stream
+    lat_plan = _lib.Plan(pupil, local)
+    lat_plan.set_spot_arrays(x[:1], y[:1], z[:1], a[:1])
+    for _ in range(3):
+        lat_plan.solve(_lib.ALG_CSWGS, ITERS, subset, th[:1], want_fields=True)
+    ls = torch.cuda.ExternalStream(lat_plan.stream(), device=torch.device("cuda", local))
+    l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    l0.record(ls)
+    for _ in range(reps):
+        lat_plan.solve(_lib.ALG_CSWGS, ITERS, subset, th[:1], want_fields=True, sync=False)
+    l1.record(ls)
+    torch.cuda.synchronize()
+    latency_ms = l0.elapsed_time(l1) / reps
+
+    # e2e through the C ABI with pinned host buffers
+    lib = _lib.load()
+    n_in = B * NSPOTS
+    h2d = 5 * n_in * 8
+    d2h = B * m * 8 + 2 * B * 8
+    bufs = {}
+    for name, count in (("x", n_in), ("y", n_in), ("z", n_in), ("a", n_in), ("th", n_in),
+                        ("ph", B * m), ("e", B), ("u", B)):
+        p = lib.hs_host_alloc(count * 8)
+        if not p:
+            raise MemoryError("cudaHostAlloc failed")
+        bufs[name] = (p, np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_double)),
+                                               shape=(count,)))
+    for name, src in (("x", x), ("y", y), ("z", z), ("a", a), ("th", th)):
+        bufs[name][1][:] = src.ravel()
+    e2e_plan = _lib.Plan(pupil, local)
+
+    def e2e_call():
+        _lib.check(lib.hs_solve_host(e2e_plan.handle, _lib.ALG_CSWGS, ITERS, subset, B, NSPOTS,
+                                     bufs["x"][0], bufs["y"][0], bufs["z"][0], bufs["a"][0],
+                                     bufs["th"][0], bufs["ph"][0], bufs["e"][0], bufs["u"][0]))
+
+    for _ in range(2):
+        e2e_call()
+    barrier()
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_call()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * B * e2e_steps / e2e_s
+    e2e_ok = bool(np.allclose(bufs["e"][1], e, rtol=0, atol=0))
+    for p, _ in bufs.values():
+        lib.hs_host_free(p)
+
+    # roofline of the dominant kernel: the full-range fused pass
+    ms_full, pairs_full = plan.time_kernel(0, reps=10)
+    ms_win, pairs_win = plan.time_kernel(1, subset, reps=50)
+    ms_upd, _ = plan.time_kernel(2, reps=50)
+    flops_full = 2 * FLOP_PER_PAIR_PASS * pairs_full
+    achieved = flops_full / (ms_full * 1e-3) / 1e12
+    peak = _lib.fma_peak_tflops(local)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("full_pass_dram_bytes_per_launch")
+    # per-step composition of kernel time (from the same per-launch timings)
+    n_full, n_win = 2, ITERS - 1
+    step_kernel_ms = n_full * ms_full + n_win * ms_win + (ITERS + 2) * ms_upd
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        rate, done, threads = cpu_oracle_rate(args.cpu_seconds)
+        cpu = {"value": rate, "unit": "holograms/s", "cores": threads, "kind": "port",
+               "sample": f"{done} holograms of the workload (CS-WGS 1152^2 N=100 I=20 + e/u), "
+               "C+OpenMP oracle bit-exact vs the reference numba kernels"}
+    pairs_step = B * NSPOTS * (2 * 2 * m + 2 * (ITERS - 1) * subset)
+    line = {
+        "metric": METRIC, "value": value, "unit": "holograms/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "ms_per_hologram": total_ms / args.steps / B,
+        "latency_ms_single_hologram": latency_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic", "config": workload_config(B),
+        "e2e": {"value": e2e_value, "unit": "holograms/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps, "matches_device_e": e2e_ok},
+        "roofline": {"bound": "fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "hs_pass_kernel<8,16,BWD|FWD> full-range fused pass",
+                     "peak_source": "measured FP32 FFMA microbenchmark (hs_fma_peak)",
+                     "algorithmic_flop_per_launch": flops_full,
+                     "ms_per_launch": ms_full,
+                     "window_pass_ms": ms_win, "update_ms": ms_upd,
+                     "step_kernel_ms_estimate": step_kernel_ms},
+        "pixel_spot_pairs_per_step": pairs_step,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk, "cpu_baseline": cpu,
+        "mean_e": float(np.mean(e)), "mean_u": float(np.mean(u)),
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

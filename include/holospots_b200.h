@@ -1,0 +1,159 @@
+/*
+ * holospots_b200.h -- C ABI of the B200-native CS-WGS hologram solver.
+ *
+ * The reference (`holospots`, pure Python + numba) has no FFI; its hot-path
+ * boundary is the module-level Python API (holospots/__init__.py:18-29).
+ * Each entry point below replaces one of those calls; the Python package
+ * `paper_2003_05293_b200` binds them with ctypes and
+ * keeps the reference signatures, argument meanings and exceptions.
+ *
+ *   hs_plan_create   <- geometry upload that the reference repeats on every
+ *                       call (Pupil arrays, optics.py:63-214)
+ *   hs_set_spots     <- spot_tables (kernels.py:177-183, _build_tables 78-96)
+ *   hs_superpose     <- superpose (kernels.py:186-214)
+ *   hs_forward       <- forward_project (kernels.py:217-246)
+ *   hs_quality       <- quality_report / spot_intensities (metrics.py:33-79)
+ *   hs_solve         <- rs / wgs / cswgs / solve (solvers.py:179-282), batched
+ *   hs_get_*         <- the (Hologram, SolverTrace) / QualityReport results
+ *
+ * Conventions
+ *   - All host arrays are plain C arrays (float64 unless noted), row-major.
+ *   - Complex values are interleaved (re, im) float64 pairs.
+ *   - Pixel arrays are in the pupil's storage order (optics.py:184-192).
+ *   - Every call is synchronous with respect to host buffers: when it
+ *     returns, host outputs are written and host inputs may be reused.
+ *     hs_solve_async is the exception (device-resident; see below).
+ *   - A plan is bound to one CUDA device and one stream; it is not
+ *     thread-safe (like the reference's process-global worker pool,
+ *     kernels.py:154-165).
+ *   - Results never depend on launch configuration, batch size or batch
+ *     position of a pattern (fixed-shape reductions), mirroring the
+ *     reference determinism contract (kernels.py:16-21).
+ *
+ * Status codes (returned by every int function; the Python layer maps them
+ * onto the holospots.errors hierarchy, errors.py:4-29):
+ */
+#ifndef HOLOSPOTS_B200_H
+#define HOLOSPOTS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HS_OK 0
+#define HS_EINVAL 1        /* InvalidParameterError */
+#define HS_EGEOMETRY 2     /* GeometryMismatchError */
+#define HS_EDEGENERATE 3   /* DegenerateFieldError: all spot fields vanished */
+#define HS_EDIVERGED 4     /* DegenerateFieldError: weights left float range */
+#define HS_ECUDA 5         /* device / launch / allocation failure */
+#define HS_EZEROILLUM 6    /* ZeroIlluminationError */
+#define HS_EUNDEFINED 7    /* UndefinedUniformityError */
+
+#define HS_ALG_RS 0
+#define HS_ALG_WGS 1
+#define HS_ALG_CSWGS 2
+
+/* hs_solve flags */
+#define HS_WANT_FIELDS 1   /* fuse the full-range e/u projection into the last pass */
+
+typedef struct hs_plan hs_plan;
+
+/* Human-readable message for the last failing call on this thread. */
+const char *hs_last_error(void);
+
+/* Number of visible CUDA devices (0 on a host without a GPU). */
+int hs_device_count(int *count);
+
+/* Largest spot count one pattern may carry. */
+int hs_max_spots(void);
+
+/* Upload pupil geometry once.  rows/cols/amplitude: m storage-order pixels;
+ * axis: side grid-line coordinates (Pupil.axis_coords, optics.py:111-115);
+ * prism/lens: Pupil.prism_coeff / lens_coeff (optics.py:101-109);
+ * sum_amplitude: Pupil.sum_amplitude (optics.py:213). */
+int hs_plan_create(int device, int side, int64_t m, const int64_t *rows,
+                   const int64_t *cols, const double *amplitude,
+                   const double *axis, double prism, double lens,
+                   double sum_amplitude, hs_plan **out);
+void hs_plan_destroy(hs_plan *plan);
+
+/* Spot targets of `batch` independent patterns with n spots each:
+ * x, y, z, a0 are [batch][n].  Builds the per-pattern phasor tables on
+ * the device (kernels.py:78-96). */
+int hs_set_spots(hs_plan *plan, int batch, int n, const double *x,
+                 const double *y, const double *z, const double *a0);
+
+/* Backward pass of pattern 0 over storage pixels [start, stop):
+ * out[stop-start] receives wrapped phases (kernels.py:186-214).
+ * amplitude/theta: [n] superposition coefficients (SpotCoefficients). */
+int hs_superpose(hs_plan *plan, const double *amplitude, const double *theta,
+                 int64_t start, int64_t stop, double *out);
+
+/* Forward pass of pattern 0: phase[m] storage order; fields[2n] receives
+ * the per-spot complex sums over [start, stop) (kernels.py:217-246). */
+int hs_forward(hs_plan *plan, const double *phase, int64_t start, int64_t stop,
+               double *fields);
+
+/* Full-range projection + metrics of pattern 0 (metrics.py:71-79):
+ * e, u scalars; intensities[n], relative[n]; fields[2n] (may be NULL). */
+int hs_quality(hs_plan *plan, const double *phase, double *e, double *u,
+               double *intensities, double *relative, double *fields);
+
+/* Run `algorithm` on all patterns of the current spot batch.
+ * iterations: I (ignored for RS); subset: ceil(c*M) for CS-WGS (M for WGS);
+ * theta0: [batch][n] starting phase offsets (solvers.py:169-170).
+ * hs_solve_async only enqueues work on the plan stream (results stay on the
+ * device; poll with hs_sync); hs_solve also waits for completion. */
+int hs_solve_async(hs_plan *plan, int algorithm, int iterations,
+                   int64_t subset, const double *theta0, int flags);
+int hs_solve(hs_plan *plan, int algorithm, int iterations, int64_t subset,
+             const double *theta0, int flags);
+int hs_sync(hs_plan *plan);
+
+/* Results of the last solve.
+ * hs_get_status: status[batch] per pattern (HS_OK / HS_EDEGENERATE /
+ *   HS_EDIVERGED), degenerate[batch] trace flags (solvers.py:116-122).
+ * hs_get_trace: weights, mags [batch][iterations][n] (StepRecord,
+ *   solvers.py:61-70).
+ * hs_get_phase: phase[count][m] for patterns first..first+count-1.
+ * hs_get_quality: e[batch], u[batch], intensities/relative [batch][n],
+ *   fields [batch][2n]; any pointer may be NULL.  Needs HS_WANT_FIELDS. */
+int hs_get_status(hs_plan *plan, int32_t *status, int32_t *degenerate);
+int hs_get_trace(hs_plan *plan, double *weights, double *mags);
+int hs_get_phase(hs_plan *plan, int first, int count, double *phase);
+int hs_get_quality(hs_plan *plan, double *e, double *u, double *intensities,
+                   double *relative, double *fields);
+
+/* End-to-end call used by bench.py's e2e leg: uploads spots + theta0 from
+ * host memory, solves, and copies phases [batch][m], e[batch], u[batch]
+ * back to host memory.  Equivalent to hs_set_spots + hs_solve +
+ * hs_get_phase + hs_get_quality. */
+int hs_solve_host(hs_plan *plan, int algorithm, int iterations, int64_t subset,
+                  int batch, int n, const double *x, const double *y,
+                  const double *z, const double *a0, const double *theta0,
+                  double *phase, double *e, double *u);
+
+/* Instrumentation for bench.py: the plan's cudaStream_t, the number of
+ * kernels the last solve launched, and the mean device time (CUDA events,
+ * `reps` back-to-back launches on the plan stream) of the kernel `which`
+ * (0 = full-range fused pass, 1 = compressed-window fused pass,
+ * 2 = weight update) with the current spot batch. */
+void *hs_plan_stream(hs_plan *plan);
+int hs_last_launch_count(hs_plan *plan, int64_t *launches);
+int hs_time_kernel(hs_plan *plan, int which, int64_t subset, int reps,
+                   double *ms_per_launch, double *pairs_per_launch);
+
+/* Measured FP32 FFMA throughput of `device` in TFLOP/s (2 FLOP per FFMA),
+ * the roofline denominator for the FMA-bound pass kernel. */
+int hs_fma_peak(int device, double *tflops);
+
+/* Page-locked host buffers for the e2e path (cudaHostAlloc / cudaFreeHost). */
+void *hs_host_alloc(int64_t bytes);
+void hs_host_free(void *ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOLOSPOTS_B200_H */

@@ -1,0 +1,277 @@
+"""ctypes binding of ``libholospots_b200.so`` (include/holospots_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, every compute entry point raises :class:`DeviceError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+import weakref
+
+import numpy as np
+
+from .errors import (DegenerateFieldError, DeviceError, GeometryMismatchError,
+                     InvalidParameterError, UndefinedUniformityError,
+                     ZeroIlluminationError)
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                        "libholospots_b200.so")
+
+HS_OK, HS_EINVAL, HS_EGEOMETRY, HS_EDEGENERATE, HS_EDIVERGED, HS_ECUDA, \
+    HS_EZEROILLUM, HS_EUNDEFINED = range(8)
+ALG_RS, ALG_WGS, ALG_CSWGS = 0, 1, 2
+WANT_FIELDS = 1
+
+_ERRORS = {
+    HS_EINVAL: InvalidParameterError,
+    HS_EGEOMETRY: GeometryMismatchError,
+    HS_EDEGENERATE: DegenerateFieldError,
+    HS_EDIVERGED: DegenerateFieldError,
+    HS_ECUDA: DeviceError,
+    HS_EZEROILLUM: ZeroIlluminationError,
+    HS_EUNDEFINED: UndefinedUniformityError,
+}
+
+# Every symbol include/holospots_b200.h declares (tests check the exports).
+EXPORTS = (
+    "hs_last_error", "hs_device_count", "hs_max_spots", "hs_plan_create",
+    "hs_plan_destroy", "hs_set_spots", "hs_superpose", "hs_forward", "hs_quality",
+    "hs_solve_async", "hs_solve", "hs_sync", "hs_get_status", "hs_get_trace",
+    "hs_get_phase", "hs_get_quality", "hs_solve_host", "hs_plan_stream",
+    "hs_last_launch_count", "hs_time_kernel", "hs_fma_peak", "hs_host_alloc",
+    "hs_host_free",
+)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load the CUDA library (raises DeviceError if it was never built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(
+                f"CUDA library not built ({LIB_PATH}); run "
+                "`python -m paper_2003_05293_b200.build` (there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        P, I, I64, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+        PP = ctypes.POINTER(ctypes.c_void_p)
+        sig = {
+            "hs_last_error": (ctypes.c_char_p, []),
+            "hs_device_count": (I, [ctypes.POINTER(I)]),
+            "hs_max_spots": (I, []),
+            "hs_plan_create": (I, [I, I, I64, P, P, P, P, D, D, D, PP]),
+            "hs_plan_destroy": (None, [P]),
+            "hs_set_spots": (I, [P, I, I, P, P, P, P]),
+            "hs_superpose": (I, [P, P, P, I64, I64, P]),
+            "hs_forward": (I, [P, P, I64, I64, P]),
+            "hs_quality": (I, [P, P, P, P, P, P, P]),
+            "hs_solve_async": (I, [P, I, I, I64, P, I]),
+            "hs_solve": (I, [P, I, I, I64, P, I]),
+            "hs_sync": (I, [P]),
+            "hs_get_status": (I, [P, P, P]),
+            "hs_get_trace": (I, [P, P, P]),
+            "hs_get_phase": (I, [P, I, I, P]),
+            "hs_get_quality": (I, [P, P, P, P, P, P]),
+            "hs_solve_host": (I, [P, I, I, I64, I, I, P, P, P, P, P, P, P, P]),
+            "hs_plan_stream": (P, [P]),
+            "hs_last_launch_count": (I, [P, ctypes.POINTER(I64)]),
+            "hs_time_kernel": (I, [P, I, I64, I, ctypes.POINTER(D), ctypes.POINTER(D)]),
+            "hs_fma_peak": (I, [I, ctypes.POINTER(D)]),
+            "hs_host_alloc": (P, [I64]),
+            "hs_host_free": (None, [P]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc != HS_OK:
+        msg = (load().hs_last_error() or b"").decode(errors="replace")
+        raise _ERRORS.get(rc, DeviceError)(msg or f"holospots_b200 status {rc}")
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    check(load().hs_device_count(ctypes.byref(n)))
+    return n.value
+
+
+def ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+_default_device = int(os.environ.get("HOLOSPOTS_DEVICE", "0"))
+
+
+def set_device(index: int) -> None:
+    """Select the CUDA device new plans bind to (one process per GPU)."""
+    global _default_device
+    _default_device = int(index)
+
+
+def get_device() -> int:
+    return _default_device
+
+
+class Plan:
+    """One pupil's geometry resident on one device (hs_plan)."""
+
+    def __init__(self, pupil, device: int | None = None):
+        lib = load()
+        if device_count() < 1:
+            raise DeviceError("no CUDA device visible; the B200 path has no CPU fallback")
+        self.device = get_device() if device is None else int(device)
+        self.m = pupil.active_count
+        self.side = pupil.side_px
+        h = ctypes.c_void_p()
+        rows = np.ascontiguousarray(pupil.rows, dtype=np.int64)
+        cols = np.ascontiguousarray(pupil.cols, dtype=np.int64)
+        amp = f64(pupil.amplitude)
+        axis = f64(pupil.axis_coords())
+        check(lib.hs_plan_create(self.device, self.side, self.m, ptr(rows), ptr(cols), ptr(amp),
+                                 ptr(axis), float(pupil.prism_coeff), float(pupil.lens_coeff),
+                                 float(pupil.sum_amplitude), ctypes.byref(h)))
+        self.handle = h
+        self._spots_key = None
+        self.batch = 0
+        self.n = 0
+        self._finalizer = weakref.finalize(self, lib.hs_plan_destroy, h)
+
+    # ---- spot batches --------------------------------------------------
+    def set_spots(self, spot_sets) -> None:
+        """Upload ``spot_sets`` (a SpotSet or a sequence of equal-size sets)."""
+        sets = list(spot_sets) if isinstance(spot_sets, (list, tuple)) else [spot_sets]
+        key = tuple(id(s) for s in sets)
+        if key == self._spots_key and all(s is not None for s in sets):
+            return
+        n = sets[0].count
+        if any(s.count != n for s in sets):
+            raise InvalidParameterError("all patterns of a batch need the same spot count")
+        x = f64(np.stack([s.x for s in sets]))
+        y = f64(np.stack([s.y for s in sets]))
+        z = f64(np.stack([s.z for s in sets]))
+        a = f64(np.stack([s.amplitude for s in sets]))
+        self.set_spot_arrays(x, y, z, a)
+        self._spots_key = key
+        self._spot_refs = sets  # keep ids stable while cached
+
+    def set_spot_arrays(self, x, y, z, a0) -> None:
+        x, y, z, a0 = (f64(np.atleast_2d(v)) for v in (x, y, z, a0))
+        b, n = x.shape
+        check(load().hs_set_spots(self.handle, b, n, ptr(x), ptr(y), ptr(z), ptr(a0)))
+        self.batch, self.n = b, n
+        self._spots_key = None
+
+    # ---- kernels --------------------------------------------------------
+    def superpose(self, amplitude, theta, start: int, stop: int) -> np.ndarray:
+        out = np.empty(stop - start, dtype=np.float64)
+        a, t = f64(amplitude), f64(theta)
+        check(load().hs_superpose(self.handle, ptr(a), ptr(t), start, stop, ptr(out)))
+        return out
+
+    def forward(self, phase, start: int, stop: int) -> np.ndarray:
+        ph = f64(phase)
+        out = np.empty(2 * self.n, dtype=np.float64)
+        check(load().hs_forward(self.handle, ptr(ph), start, stop, ptr(out)))
+        return out[0::2] + 1j * out[1::2]
+
+    def quality(self, phase):
+        ph = f64(phase)
+        e, u = ctypes.c_double(), ctypes.c_double()
+        inten = np.empty(self.n)
+        rel = np.empty(self.n)
+        fields = np.empty(2 * self.n)
+        check(load().hs_quality(self.handle, ptr(ph), ctypes.byref(e), ctypes.byref(u),
+                                ptr(inten), ptr(rel), ptr(fields)))
+        return e.value, u.value, inten, rel, fields[0::2] + 1j * fields[1::2]
+
+    # ---- solver ---------------------------------------------------------
+    def solve(self, algorithm: int, iterations: int, subset: int, theta0,
+              want_fields: bool = True, sync: bool = True) -> None:
+        th = f64(theta0)
+        fn = load().hs_solve if sync else load().hs_solve_async
+        check(fn(self.handle, algorithm, iterations, subset, ptr(th),
+                 WANT_FIELDS if want_fields else 0))
+
+    def sync(self) -> None:
+        check(load().hs_sync(self.handle))
+
+    def status(self):
+        st = np.zeros(self.batch, dtype=np.int32)
+        dg = np.zeros(self.batch, dtype=np.int32)
+        check(load().hs_get_status(self.handle, ptr(st), ptr(dg)))
+        return st, dg
+
+    def trace(self, iterations: int):
+        w = np.empty((self.batch, iterations, self.n))
+        m = np.empty((self.batch, iterations, self.n))
+        if iterations:
+            check(load().hs_get_trace(self.handle, ptr(w), ptr(m)))
+        return w, m
+
+    def phases(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        count = self.batch - first if count is None else count
+        out = np.empty((count, self.m), dtype=np.float64)
+        check(load().hs_get_phase(self.handle, first, count, ptr(out)))
+        return out
+
+    def quality_batch(self):
+        b, n = self.batch, self.n
+        e, u = np.empty(b), np.empty(b)
+        inten, rel, fields = np.empty((b, n)), np.empty((b, n)), np.empty((b, 2 * n))
+        check(load().hs_get_quality(self.handle, ptr(e), ptr(u), ptr(inten), ptr(rel),
+                                    ptr(fields)))
+        return e, u, inten, rel, fields[:, 0::2] + 1j * fields[:, 1::2]
+
+    def stream(self) -> int:
+        return int(load().hs_plan_stream(self.handle) or 0)
+
+    def last_launch_count(self) -> int:
+        v = ctypes.c_int64()
+        check(load().hs_last_launch_count(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def time_kernel(self, which: int, subset: int = 0, reps: int = 20):
+        ms, pairs = ctypes.c_double(), ctypes.c_double()
+        check(load().hs_time_kernel(self.handle, which, subset, reps, ctypes.byref(ms),
+                                    ctypes.byref(pairs)))
+        return ms.value, pairs.value
+
+
+def fma_peak_tflops(device: int | None = None) -> float:
+    """Measured FP32 FFMA peak of the device (TFLOP/s)."""
+    v = ctypes.c_double()
+    check(load().hs_fma_peak(get_device() if device is None else int(device), ctypes.byref(v)))
+    return v.value
+
+
+_plans: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def plan_for(pupil, device: int | None = None) -> Plan:
+    """The cached device plan of ``pupil`` (geometry uploaded once)."""
+    dev = get_device() if device is None else int(device)
+    per = _plans.get(pupil)
+    if per is None:
+        per = {}
+        _plans[pupil] = per
+    plan = per.get(dev)
+    if plan is None:
+        plan = Plan(pupil, dev)
+        per[dev] = plan
+    return plan
