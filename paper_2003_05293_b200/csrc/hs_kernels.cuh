@@ -1,22 +1,35 @@
 // hs_kernels.cuh -- sm_100a device kernels of the CS-WGS hot path.
 //
 //   hs_tables_kernel  per-pattern column/row unit phasors gx, gy
-//                     (reference _build_tables, holospots/kernels.py:78-96)
-//   hs_pass_kernel    fused pixel pass over a pixel list: back-propagation
-//                     S_p = sum_n coef_n gx[c_p,n] gy[r_p,n] -> arg (kernels.py:99-119)
-//                     and/or forward projection E_n += b_p gx gy with
-//                     b_p = A_p e^{-i arg S_p} (kernels.py:122-144), one
-//                     deterministic partial per (pattern, chunk)
-//   hs_update_kernel  fixed-order fp64 fold of the chunk partials + the
-//                     weight / theta update (solvers.py:96-163) or the
-//                     e / u epilogue (metrics.py:33-79)
+//                     (reference _build_tables, holospots/kernels.py:78-96),
+//                     optionally fused with the seed coefficients
+//                     (solvers.py:166-176, kernels.py:206-208)
+//   hs_seed_kernel    superposition coefficients a e^{i wrap(theta)}
+//   hs_pass_kernel    fused pixel pass over a pixel list:
+//                       back-propagation S_p = sum_n coef_n gy[r_p,n] gx[c_p,n]
+//                       -> arg S_p (kernels.py:99-119), and/or
+//                       forward projection E_n += b_p gx[c_p,n] gy[r_p,n] with
+//                       b_p = A_p e^{-i arg S_p} (kernels.py:122-144);
+//                     then a two-level fixed-order fold of the per-CTA partials
+//                     done by the last CTA of each group / pattern, which also
+//                     runs the weight / theta update (solvers.py:104-163) or the
+//                     e / u epilogue (metrics.py:33-79) -- one launch per
+//                     solver iteration.
 //
-// Numerics: phasor arguments are formed in fp64 in the
-// reference's operation order (no FMA contraction) and rounded to fp32
-// phasors; the pixel loops run in fp32 on the FMA pipe; every reduction
-// across pixels is a fixed-shape tree whose shape depends only on the list
-// length, never on scheduling, so results are bitwise run-to-run stable and
-// independent of batch size.
+// Work decomposition.  G lanes cooperate on one pixel;
+// lane g owns spots {2g, 2g+1} + 2G*j (j < nl/2) so table rows are read as
+// float4.  A warp holds SPW = 32/G pixel slots.  Each slot walks a run of
+// list entries; while the row stays the same it keeps V = coef * gy[row]
+// (backward) and T = sum b_p gx[c_p] (forward) in registers, so a pixel
+// costs one gx row read + 8 FFMA per spot, and a row change costs one gy
+// row read.  Dense (full-range) lists are laid out so the SPW slots of a warp
+// sit on SPW rows of the same column(s): the gx row load is a broadcast.
+//
+// Numerics: phasor arguments are formed in fp64 in the reference's order
+// (no FMA contraction) and rounded to fp32 phasors; pixel loops run in fp32
+// on the FMA pipe; every cross-pixel reduction has a fixed shape that
+// depends only on the list layout, so results are bitwise reproducible and
+// independent of the batch size and of CTA scheduling.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -24,44 +37,92 @@
 
 namespace hs {
 
-constexpr int kThreads = 256;        // pass-kernel CTA size
-constexpr int kTargetChunks = 296;   // 2 x 148 SMs: chunks per pattern and pass
-constexpr int kUpdThreads = 1024;
+constexpr int kThreads = 256;        // pass-kernel CTA size (8 warps)
+constexpr int kWarps = kThreads / 32;
+constexpr int kTargetChunks = 296;   // sparse lists: chunks per pattern (2 x 148 SMs)
+constexpr int kGroup = 32;           // chunks per first-level fold group
 constexpr double kPi = 3.141592653589793;
 constexpr double kTwoPi = 6.283185307179586;
 
 enum PassMode : int { PM_BWD = 1, PM_FWD = 2, PM_WRITE = 4 };
+enum FoldAct : int { ACT_NONE = 0, ACT_STEP = 1, ACT_FINAL = 2, ACT_FIELDS = 3 };
+
+struct UpdArgs {
+    int act;                  // FoldAct
+    int n, np;
+    const double *a0;         // [B][n] target amplitudes
+    double *w;                // [B][np] weights
+    float2 *coef;             // [B][np] coefficients for the next pass
+    double *trace_w, *trace_m;  // [B][iters][n]
+    int iter, iters;
+    int32_t *status, *degen, *qstatus;  // [B]
+    double *fields;           // [B][n][2]
+    double inv_norm;          // 1 / sum_amplitude^2
+    double *e, *u, *inten, *rel;  // [B], [B], [B][n], [B][n]
+};
 
 struct PassArgs {
     const int32_t *rc;        // packed (row << 16) | col per list entry
-    const float *amp;         // illumination amplitude per entry
-    const int32_t *dst;       // phase index per entry (nullptr: i + idx_base)
+    const float *amp;         // illumination amplitude per entry (0: padding)
+    const int32_t *dst;       // storage index per entry, -1 padding (nullptr: i + idx_base)
     int64_t idx_base;
     int64_t count;            // list length
-    int32_t chunk_len;        // entries per CTA (multiple of the slot count)
-    int32_t side;
-    int32_t np;               // padded spot count (G * spots-per-lane)
+    int32_t chunk_len;        // entries per CTA; multiple of 8 * SPW
+    int32_t nchunks;
+    int32_t np, nl;           // padded spot count, spots per lane (even)
     int64_t tab_stride;       // side * np
     const float2 *gx, *gy;    // [B][side][np]
-    const float2 *coef;       // [B][np]   superposition coefficients
+    const float2 *coef;       // [B][np]
     const double *phase_in;   // [B][phase_stride] (PM_FWD without PM_BWD)
     double *phase_out;        // [B][phase_stride] (PM_WRITE)
     int64_t phase_stride;
     float2 *partials;         // [B][part_stride]: [chunk][np]
     int64_t part_stride;
-    const int32_t *status;    // [B] nonzero -> pattern already failed, skip
+    double2 *gpart;           // [B][gpart_stride]: [group][np]
+    int64_t gpart_stride;
+    int32_t *grp_cnt;         // [B][cnt_stride] arrival counters (self-resetting)
+    int32_t *pat_cnt;         // [B]
+    int32_t cnt_stride;
+    UpdArgs u;
 };
 
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ double hs_wrap(double t)
+{
+    // optics.py:31-45: exact fmod, then one exact +-2pi correction.
+    double w = fmod(t, kTwoPi);
+    if (w >= kPi) w -= kTwoPi;
+    if (w < -kPi) w += kTwoPi;
+    return w;
+}
+
+__device__ __forceinline__ void hs_seed_one(int b, int k, int n, int np, const double *amp,
+                                            const double *theta, float2 *coef, double *w)
+{
+    float2 c = make_float2(0.f, 0.f);
+    double wk = 0.0;
+    if (k < n) {
+        const double th = hs_wrap(theta[(int64_t)b * n + k]);
+        const double am = amp[(int64_t)b * n + k];
+        double s, co;
+        sincos(th, &s, &co);
+        c = make_float2((float)(am * co), (float)(am * s));
+        wk = 1.0;
+    }
+    coef[(int64_t)b * np + k] = c;
+    if (w) w[(int64_t)b * np + k] = wk;
+}
+
 // Tables: gx[b][j][n] = exp(i (c1 x_n a_j + c2 z_n a_j^2)), gy likewise with
-// y_n.  The argument is formed with explicit round-to-nearest fp64 ops in the
-// reference order ((c1*x)*v + (c2*z)*v2), so it equals numba's argument bit
-// for bit; sincos runs in fp64 and the phasor is rounded once to fp32.
-// ---------------------------------------------------------------------------
+// y_n; the argument is formed with explicit round-to-nearest fp64 ops in the
+// reference order ((c1*x)*v + (c2*z)*v2) -> numba's bits; fp64 sincos; one
+// rounding to fp32.  Block (0, b) also seeds pattern b when seed_theta != 0.
 __global__ void hs_tables_kernel(int side, int np, int n, const double *__restrict__ axis,
                                  double c1, double c2, const double *__restrict__ x,
                                  const double *__restrict__ y, const double *__restrict__ z,
-                                 float2 *__restrict__ gx, float2 *__restrict__ gy)
+                                 float2 *__restrict__ gx, float2 *__restrict__ gy,
+                                 const double *seed_amp, const double *seed_theta,
+                                 float2 *coef, double *w)
 {
     const int j = blockIdx.x;
     const int b = blockIdx.y;
@@ -84,191 +145,25 @@ __global__ void hs_tables_kernel(int side, int np, int n, const double *__restri
         }
         gx[row + k] = px;
         gy[row + k] = py;
+        if (j == 0 && seed_theta != nullptr) hs_seed_one(b, k, n, np, seed_amp, seed_theta, coef, w);
     }
 }
 
-// ---------------------------------------------------------------------------
-// Fused pixel pass.  G lanes cooperate on one pixel; lane g owns spots
-// n = g + G*k (k < L), so a group's table reads are contiguous.  Each CTA
-// owns chunk blockIdx.x of the list ([chunk_len] consecutive entries) for
-// pattern blockIdx.y and writes one partial per spot: the per-lane fp32 sums
-// are folded over the CTA's pixel slots in slot order.
-// ---------------------------------------------------------------------------
-template <int G, int L, int MODE>
-__global__ void __launch_bounds__(kThreads, (L > 16 ? 1 : 2))
-hs_pass_kernel(const PassArgs a)
+__global__ void hs_seed_kernel(int n, int np, const double *amp, const double *theta, float2 *coef,
+                               double *w)
 {
-    constexpr int NSLOTS = kThreads / G;
-    constexpr bool BWD = (MODE & PM_BWD) != 0;
-    constexpr bool FWD = (MODE & PM_FWD) != 0;
-    constexpr bool WRITE = (MODE & PM_WRITE) != 0;
-    extern __shared__ float2 red[];  // [NSLOTS][np]
-
-    const int pat = blockIdx.y;
-    if (a.status != nullptr && a.status[pat] != 0) return;  // uniform per CTA
-
-    const int tid = threadIdx.x;
-    const int g = tid % G;
-    const int slot = tid / G;
-    const int np = a.np;
-    const int nl = np / G;
-    const float2 *__restrict__ gxp = a.gx + (int64_t)pat * a.tab_stride + g;
-    const float2 *__restrict__ gyp = a.gy + (int64_t)pat * a.tab_stride + g;
-
-    float cr[L], ci[L], er[L], ei[L];
-#pragma unroll
-    for (int k = 0; k < L; ++k) {
-        cr[k] = 0.f; ci[k] = 0.f; er[k] = 0.f; ei[k] = 0.f;
-        if (BWD && k < nl) {
-            const float2 c = a.coef[(int64_t)pat * np + g + G * k];
-            cr[k] = c.x; ci[k] = c.y;
-        }
-    }
-
-    const int64_t begin = (int64_t)blockIdx.x * a.chunk_len;
-    int64_t end = begin + a.chunk_len;
-    if (end > a.count) end = a.count;
-    const int trips = (int)((end - begin + NSLOTS - 1) / NSLOTS);
-
-    for (int t = 0; t < trips; ++t) {
-        const int64_t i = begin + (int64_t)t * NSLOTS + slot;
-        const bool valid = i < end;
-        int rc = 0;
-        float A = 0.f;
-        if (valid) { rc = __ldg(a.rc + i); A = __ldg(a.amp + i); }
-        const int r = rc >> 16, c = rc & 0xffff;
-        const float2 *__restrict__ px = gxp + (int64_t)c * np;
-        const float2 *__restrict__ py = gyp + (int64_t)r * np;
-
-        float pr[L], pi[L];
-        float sr = 0.f, si = 0.f;
-#pragma unroll
-        for (int k = 0; k < L; ++k) {
-            pr[k] = 0.f; pi[k] = 0.f;
-            if (k < nl) {
-                const float2 u = __ldg(px + G * k);
-                const float2 v = __ldg(py + G * k);
-                pr[k] = u.x * v.x - u.y * v.y;
-                pi[k] = u.x * v.y + u.y * v.x;
-                if (BWD) {
-                    sr += cr[k] * pr[k] - ci[k] * pi[k];
-                    si += cr[k] * pi[k] + ci[k] * pr[k];
-                }
-            }
-        }
-
-        float br, bi;
-        if (BWD) {
-            // Butterfly over the G lanes of the pixel; a+b == b+a, so every
-            // lane ends with the same bits.
-#pragma unroll
-            for (int o = G / 2; o > 0; o >>= 1) {
-                sr += __shfl_xor_sync(0xffffffffu, sr, o);
-                si += __shfl_xor_sync(0xffffffffu, si, o);
-            }
-            // b = A e^{-i arg S} = A conj(S)/|S|; arg(0) = 0 (kernels.py:115-119).
-            const float m2 = sr * sr + si * si;
-            if (m2 > 0.f && m2 < INFINITY) {
-                const float inv = rsqrtf(m2);
-                br = A * (sr * inv);
-                bi = -A * (si * inv);
-            } else if (sr != 0.f || si != 0.f) {
-                const float mx = fmaxf(fabsf(sr), fabsf(si));
-                const float xr = sr / mx, xi = si / mx;
-                const float inv = rsqrtf(xr * xr + xi * xi);
-                br = A * (xr * inv);
-                bi = -A * (xi * inv);
-            } else {
-                br = A;
-                bi = 0.f;
-            }
-            if (WRITE && valid && g == 0) {
-                double ph = 0.0;
-                if (sr != 0.f || si != 0.f) {
-                    ph = (double)atan2f(si, sr);
-                    if (ph >= kPi) ph -= kTwoPi;        // pi -> -pi convention
-                    else if (ph < -kPi) ph += kTwoPi;   // fp32 -pi below fp64 -pi
-                }
-                const int64_t di = a.dst ? (int64_t)a.dst[i] : i + a.idx_base;
-                a.phase_out[(int64_t)pat * a.phase_stride + di] = ph;
-            }
-        } else {
-            double s = 0.0, co = 1.0;
-            if (valid) {
-                const int64_t di = a.dst ? (int64_t)a.dst[i] : i + a.idx_base;
-                sincos(a.phase_in[(int64_t)pat * a.phase_stride + di], &s, &co);
-            }
-            br = A * (float)co;
-            bi = -A * (float)s;
-        }
-
-        if (FWD) {
-#pragma unroll
-            for (int k = 0; k < L; ++k) {
-                er[k] += br * pr[k] - bi * pi[k];
-                ei[k] += br * pi[k] + bi * pr[k];
-            }
-        }
-    }
-
-    if (FWD) {
-#pragma unroll
-        for (int k = 0; k < L; ++k)
-            if (k < nl) red[slot * np + g + G * k] = make_float2(er[k], ei[k]);
-        __syncthreads();
-        float2 *out = a.partials + (int64_t)pat * a.part_stride + (int64_t)blockIdx.x * np;
-        for (int n = tid; n < np; n += kThreads) {
-            float sx = 0.f, sy = 0.f;
-            for (int s = 0; s < NSLOTS; ++s) {
-                const float2 v = red[s * np + n];
-                sx += v.x;
-                sy += v.y;
-            }
-            out[n] = make_float2(sx, sy);
-        }
-    }
+    for (int k = threadIdx.x; k < np; k += blockDim.x) hs_seed_one(blockIdx.x, k, n, np, amp, theta, coef, w);
 }
 
 // ---------------------------------------------------------------------------
-// Update / epilogue kernel: one CTA per pattern.
-// ---------------------------------------------------------------------------
-enum UpdMode : int { UPD_SEED = 0, UPD_STEP = 1, UPD_FINAL = 2, UPD_FIELDS = 3 };
-
-struct UpdArgs {
-    int mode;
-    int n, np, nchunks;
-    const float2 *partials;
-    int64_t part_stride;
-    const double *amp_in;     // [B][n] SEED: amplitudes
-    const double *theta_in;   // [B][n] SEED: phase offsets
-    const double *a0;         // [B][n] target amplitudes
-    double *w;                // [B][np] weights
-    float2 *coef;             // [B][np]
-    double *trace_w, *trace_m;  // [B][iters][n]
-    int iter, iters;
-    int32_t *status, *degen, *qstatus;  // [B]
-    double *fields;           // [B][n][2]
-    double inv_norm;          // 1 / sum_amplitude^2
-    double *e, *u, *inten, *rel;  // [B], [B], [B][n], [B][n]
-};
-
-__device__ __forceinline__ double hs_wrap(double t)
-{
-    // optics.py:31-45: exact fmod then one exact +-2pi correction.
-    double w = fmod(t, kTwoPi);
-    if (w >= kPi) w -= kTwoPi;
-    if (w < -kPi) w += kTwoPi;
-    return w;
-}
-
-// Fixed-shape tree reductions over kUpdThreads values in shared memory.
+// Fixed-shape block reductions over kThreads values.
 template <typename T, typename Op>
-__device__ __forceinline__ T hs_block_tree(T *buf, T v, Op op)
+__device__ __forceinline__ T hs_tree(T *buf, T v, Op op)
 {
     const int tid = threadIdx.x;
     buf[tid] = v;
     __syncthreads();
-    for (int s = kUpdThreads / 2; s > 0; s >>= 1) {
+    for (int s = kThreads / 2; s > 0; s >>= 1) {
         if (tid < s) buf[tid] = op(buf[tid], buf[tid + s]);
         __syncthreads();
     }
@@ -277,97 +172,42 @@ __device__ __forceinline__ T hs_block_tree(T *buf, T v, Op op)
     return r;
 }
 
-__global__ void __launch_bounds__(kUpdThreads) hs_update_kernel(const UpdArgs a)
+struct DSum { __device__ double operator()(double p, double q) const { return p + q; } };
+struct DMin { __device__ double operator()(double p, double q) const { return fmin(p, q); } };
+struct DMax { __device__ double operator()(double p, double q) const { return fmax(p, q); } };
+struct ISum { __device__ int operator()(int p, int q) const { return p + q; } };
+
+// The pattern's fields E (fp64, in shared memory) -> action.  Runs in the
+// last CTA of the pattern with all kThreads threads.
+__device__ __forceinline__ void hs_update(const UpdArgs &a, int b, double2 *E, double *mag_s,
+                                       double *dbuf, int *ibuf)
 {
-    __shared__ double2 fold[kUpdThreads];
-    __shared__ double dbuf[kUpdThreads];
-    __shared__ int ibuf[kUpdThreads];
-    const int b = blockIdx.x;
     const int tid = threadIdx.x;
     const int n = a.n, np = a.np;
-    if (a.status[b] != 0) return;
-
-    if (a.mode == UPD_SEED) {
-        for (int k = tid; k < np; k += kUpdThreads) {
-            float2 c = make_float2(0.f, 0.f);
-            double w = 0.0;
-            if (k < n) {
-                const double th = hs_wrap(a.theta_in[(int64_t)b * n + k]);
-                const double am = a.amp_in[(int64_t)b * n + k];
-                double s, co;
-                sincos(th, &s, &co);
-                c = make_float2((float)(am * co), (float)(am * s));
-                w = 1.0;
+    if (a.act == ACT_FIELDS || a.act == ACT_FINAL) {
+        double esum = 0.0, hi = -INFINITY, lo = INFINITY;
+        for (int k = tid; k < n; k += kThreads) {
+            const double er = E[k].x, ei = E[k].y;
+            a.fields[((int64_t)b * n + k) * 2 + 0] = er;
+            a.fields[((int64_t)b * n + k) * 2 + 1] = ei;
+            if (a.act == ACT_FINAL) {
+                const double I = (er * er + ei * ei) * a.inv_norm;   // metrics.py:33-42
+                const double t0 = a.a0[(int64_t)b * n + k];
+                const double rl = I / (t0 * t0);                     // metrics.py:65-68
+                a.inten[(int64_t)b * n + k] = I;
+                a.rel[(int64_t)b * n + k] = rl;
+                esum += I;
+                hi = fmax(hi, rl);
+                lo = fmin(lo, rl);
             }
-            a.coef[(int64_t)b * np + k] = c;
-            if (a.w) a.w[(int64_t)b * np + k] = w;
         }
-        return;
-    }
-
-    // 1) fold the chunk partials: R ranges per spot, each summed in chunk
-    //    order in fp64, then the R range sums in range order.
-    int R = kUpdThreads / np;
-    if (R < 1) R = 1;
-    if (R > a.nchunks) R = a.nchunks;
-    const int cpr = (a.nchunks + R - 1) / R;
-    const float2 *part = a.partials + (int64_t)b * a.part_stride;
-    for (int t = tid; t < R * np; t += kUpdThreads) {
-        const int r = t / np, k = t % np;
-        const int c0 = r * cpr;
-        int c1 = c0 + cpr;
-        if (c1 > a.nchunks) c1 = a.nchunks;
-        double sx = 0.0, sy = 0.0;
-        int c = c0;
-        for (; c + 4 <= c1; c += 4) {
-            const float2 v0 = part[(int64_t)(c + 0) * np + k];
-            const float2 v1 = part[(int64_t)(c + 1) * np + k];
-            const float2 v2 = part[(int64_t)(c + 2) * np + k];
-            const float2 v3 = part[(int64_t)(c + 3) * np + k];
-            sx += (double)v0.x; sy += (double)v0.y;
-            sx += (double)v1.x; sy += (double)v1.y;
-            sx += (double)v2.x; sy += (double)v2.y;
-            sx += (double)v3.x; sy += (double)v3.y;
-        }
-        for (; c < c1; ++c) {
-            const float2 v = part[(int64_t)c * np + k];
-            sx += (double)v.x; sy += (double)v.y;
-        }
-        fold[t] = make_double2(sx, sy);
-    }
-    __syncthreads();
-    double er = 0.0, ei = 0.0;
-    const bool live = tid < n;
-    if (live) {
-        for (int r = 0; r < R; ++r) {
-            er += fold[r * np + tid].x;
-            ei += fold[r * np + tid].y;
-        }
-    }
-    __syncthreads();
-
-    if (a.mode == UPD_FIELDS || a.mode == UPD_FINAL) {
-        if (live) {
-            a.fields[((int64_t)b * n + tid) * 2 + 0] = er;
-            a.fields[((int64_t)b * n + tid) * 2 + 1] = ei;
-        }
-        if (a.mode == UPD_FIELDS) return;
-        // metrics.py:33-62
-        const double I = live ? (er * er + ei * ei) * a.inv_norm : 0.0;
-        const double t0 = live ? a.a0[(int64_t)b * n + tid] : 1.0;
-        const double rl = I / (t0 * t0);
-        if (live) {
-            a.inten[(int64_t)b * n + tid] = I;
-            a.rel[(int64_t)b * n + tid] = rl;
-        }
-        const double esum = hs_block_tree(dbuf, I, [](double p, double q) { return p + q; });
-        const double hi = hs_block_tree(dbuf, live ? rl : -INFINITY,
-                                        [](double p, double q) { return fmax(p, q); });
-        const double lo = hs_block_tree(dbuf, live ? rl : INFINITY,
-                                        [](double p, double q) { return fmin(p, q); });
+        if (a.act == ACT_FIELDS) return;
+        esum = hs_tree(dbuf, esum, DSum());                          // metrics.py:45-50
+        hi = hs_tree(dbuf, hi, DMax());
+        lo = hs_tree(dbuf, lo, DMin());
         if (tid == 0) {
             a.e[b] = esum;
-            if (hi == 0.0) {
+            if (hi == 0.0) {                                         // metrics.py:53-62
                 a.u[b] = 0.0;
                 a.qstatus[b] = 7;  // HS_EUNDEFINED
             } else {
@@ -377,47 +217,308 @@ __global__ void __launch_bounds__(kUpdThreads) hs_update_kernel(const UpdArgs a)
         }
         return;
     }
-
-    // 2) UPD_STEP: rebalance_weights (solvers.py:104-129) + coefficient
-    //    update (solvers.py:148-151, kernels.py:206-208).
-    double mag = live ? hypot(er, ei) : 0.0;
-    const int zeros = hs_block_tree(ibuf, (live && mag == 0.0) ? 1 : 0,
-                                    [](int p, int q) { return p + q; });
+    // ACT_STEP: rebalance_weights (solvers.py:104-129), then the coefficient
+    // update a = w a0, theta = arg E (solvers.py:148-151, kernels.py:206-208).
+    int zeros = 0;
+    double minpos = INFINITY;
+    for (int k = tid; k < n; k += kThreads) {
+        const double m = hypot(E[k].x, E[k].y);
+        mag_s[k] = m;
+        if (m == 0.0) ++zeros;
+        else minpos = fmin(minpos, m);
+    }
+    zeros = hs_tree(ibuf, zeros, ISum());
     if (zeros > 0) {
-        const double minpos = hs_block_tree(dbuf, (live && mag > 0.0) ? mag : INFINITY,
-                                            [](double p, double q) { return fmin(p, q); });
+        minpos = hs_tree(dbuf, minpos, DMin());
         if (minpos == INFINITY) {
             if (tid == 0) a.status[b] = 3;  // HS_EDEGENERATE
             return;
         }
-        if (live && mag == 0.0) mag = minpos * 1e-6;  // DEGENERACY_FLOOR
-        if (tid == 0 && a.degen[b] == 0) a.degen[b] = a.iter + 1;  // first degenerate step
+        for (int k = tid; k < n; k += kThreads)
+            if (mag_s[k] == 0.0) mag_s[k] = minpos * 1e-6;  // DEGENERACY_FLOOR
+        if (tid == 0 && a.degen[b] == 0) a.degen[b] = a.iter + 1;
     }
-    const double msum = hs_block_tree(dbuf, live ? mag : 0.0,
-                                      [](double p, double q) { return p + q; });
+    double msum = 0.0;
+    for (int k = tid; k < n; k += kThreads) msum += mag_s[k];
+    msum = hs_tree(dbuf, msum, DSum());
     const double mean = msum / (double)n;
-    double w = 0.0;
-    if (live) w = a.w[(int64_t)b * np + tid] * (mean / mag);
-    const int bad = hs_block_tree(ibuf, (live && !isfinite(w)) ? 1 : 0,
-                                  [](int p, int q) { return p + q; });
+    int bad = 0;
+    for (int k = tid; k < n; k += kThreads) {
+        const double wk = a.w[(int64_t)b * np + k] * (mean / mag_s[k]);
+        if (!isfinite(wk)) ++bad;
+        mag_s[k + np] = wk;  // stash (mag_s has 2*np doubles)
+    }
+    bad = hs_tree(ibuf, bad, ISum());
     if (bad > 0) {
         if (tid == 0) a.status[b] = 4;  // HS_EDIVERGED
         return;
     }
-    if (live) {
-        const int64_t tix = ((int64_t)b * a.iters + a.iter) * n + tid;
-        a.trace_w[tix] = w;
-        a.trace_m[tix] = mag;
-        a.w[(int64_t)b * np + tid] = w;
-        const double am = w * a.a0[(int64_t)b * n + tid];
-        double th = 0.0;
+    for (int k = tid; k < n; k += kThreads) {
+        const double wk = mag_s[k + np];
+        const int64_t tix = ((int64_t)b * a.iters + a.iter) * n + k;
+        a.trace_w[tix] = wk;
+        a.trace_m[tix] = mag_s[k];
+        a.w[(int64_t)b * np + k] = wk;
+        const double am = wk * a.a0[(int64_t)b * n + k];
+        const double er = E[k].x, ei = E[k].y;
+        double th = 0.0;                                   // solvers.py:96-101
         if (er != 0.0 || ei != 0.0) {
             th = atan2(ei, er);
             if (th == kPi) th = -kPi;
         }
         double s, co;
         sincos(th, &s, &co);
-        a.coef[(int64_t)b * np + tid] = make_float2((float)(am * co), (float)(am * s));
+        a.coef[(int64_t)b * np + k] = make_float2((float)(am * co), (float)(am * s));
+    }
+}
+
+// Two-level fold run after a CTA has written its chunk partial.  The last CTA
+// of each kGroup-chunk group folds the group in chunk order (fp64); the last
+// group-folder of the pattern folds the groups in order and applies the
+// action.  Counters reset themselves, so graphs replay without memsets.
+__device__ __forceinline__ void hs_fold(const PassArgs &a, int pat, int chunk, char *scratch)
+{
+    __shared__ int s_last;
+    __shared__ double dbuf[kThreads];
+    __shared__ int ibuf[kThreads];
+    const int tid = threadIdx.x;
+    const int np = a.np;
+    const int ngroups = (a.nchunks + kGroup - 1) / kGroup;
+    const int grp = chunk / kGroup;
+    const int c0 = grp * kGroup;
+    const int c1 = min(c0 + kGroup, a.nchunks);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        const int t = atomicAdd(a.grp_cnt + (int64_t)pat * a.cnt_stride + grp, 1);
+        s_last = (t == c1 - c0 - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const float2 *part = a.partials + (int64_t)pat * a.part_stride;
+    double2 *gp = a.gpart + (int64_t)pat * a.gpart_stride;
+    for (int k = tid; k < np; k += kThreads) {
+        double sx = 0.0, sy = 0.0;
+        for (int c = c0; c < c1; ++c) {
+            const float2 v = __ldcg(part + (int64_t)c * np + k);
+            sx += (double)v.x;
+            sy += (double)v.y;
+        }
+        gp[(int64_t)grp * np + k] = make_double2(sx, sy);
+    }
+    if (tid == 0) a.grp_cnt[(int64_t)pat * a.cnt_stride + grp] = 0;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        const int t = atomicAdd(a.pat_cnt + pat, 1);
+        s_last = (t == ngroups - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (tid == 0) a.pat_cnt[pat] = 0;
+    double2 *E = reinterpret_cast<double2 *>(scratch);           // [np]
+    double *mag_s = reinterpret_cast<double *>(E + np);           // [2*np]
+    for (int k = tid; k < np; k += kThreads) {
+        double sx = 0.0, sy = 0.0;
+        for (int gI = 0; gI < ngroups; ++gI) {
+            const double2 v = __ldcg(gp + (int64_t)gI * np + k);
+            sx += v.x;
+            sy += v.y;
+        }
+        E[k] = make_double2(sx, sy);
+    }
+    __syncthreads();
+    hs_update(a.u, pat, E, mag_s, dbuf, ibuf);
+}
+
+// ---------------------------------------------------------------------------
+template <int G, int NL, int MODE>
+__global__ void __launch_bounds__(kThreads, (NL > 16 ? 1 : 2))
+hs_pass_kernel(const PassArgs a)
+{
+    constexpr int SPW = 32 / G;
+    constexpr int NSLOT = kThreads / G;
+    constexpr int NV = NL / 2;
+    constexpr bool BWD = (MODE & PM_BWD) != 0;
+    constexpr bool FWD = (MODE & PM_FWD) != 0;
+    constexpr bool WRITE = (MODE & PM_WRITE) != 0;
+    extern __shared__ float4 smem4[];
+
+    const int pat = blockIdx.y;
+    const int chunk = blockIdx.x;
+    if (a.u.status[pat] != 0) return;  // pattern already failed (uniform per CTA)
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int g = lane % G, s = lane / G;
+    const int slot = warp * SPW + s;
+    const int npv = a.np >> 1;     // float4 per table row
+    const int nv = a.nl >> 1;      // active float4 per lane
+    float4 *coef_s = smem4;                  // [npv]
+    float4 *E_s = smem4 + npv;               // [NSLOT][npv]
+
+    if (BWD) {
+        const float4 *cg = reinterpret_cast<const float4 *>(a.coef + (int64_t)pat * a.np);
+        for (int k = tid; k < npv; k += kThreads) coef_s[k] = cg[k];
+    }
+    if (FWD)
+        for (int k = tid; k < NSLOT * npv; k += kThreads) E_s[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+
+    const float4 *__restrict__ X = reinterpret_cast<const float4 *>(a.gx + (int64_t)pat * a.tab_stride) + g;
+    const float4 *__restrict__ Y = reinterpret_cast<const float4 *>(a.gy + (int64_t)pat * a.tab_stride) + g;
+
+    float vr[NL], vi[NL], tr[NL], ti[NL];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) { vr[k] = 0.f; vi[k] = 0.f; tr[k] = 0.f; ti[k] = 0.f; }
+
+    auto flush = [&](int r) {
+        // E_slot += gy[r] * T, T = 0
+        const float4 *yr = Y + (int64_t)r * npv;
+        float4 *es = E_s + slot * npv + g;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            if (j < nv) {
+                const float4 q = __ldg(yr + G * j);
+                float4 e = es[G * j];
+                e.x += q.x * tr[2 * j] - q.y * ti[2 * j];
+                e.y += q.x * ti[2 * j] + q.y * tr[2 * j];
+                e.z += q.z * tr[2 * j + 1] - q.w * ti[2 * j + 1];
+                e.w += q.z * ti[2 * j + 1] + q.w * tr[2 * j + 1];
+                es[G * j] = e;
+            }
+            tr[2 * j] = 0.f; ti[2 * j] = 0.f; tr[2 * j + 1] = 0.f; ti[2 * j + 1] = 0.f;
+        }
+    };
+
+    const int64_t begin = (int64_t)chunk * a.chunk_len;
+    const int wseg = a.chunk_len / kWarps;
+    const int64_t wbegin = begin + (int64_t)warp * wseg;
+    int64_t wend = wbegin + wseg;
+    if (wend > a.count) wend = a.count;
+    const int trips = (wend > wbegin) ? (int)((wend - wbegin + SPW - 1) / SPW) : 0;
+    int rcur = -1;
+
+    for (int t = 0; t < trips; ++t) {
+        const int64_t i = wbegin + (int64_t)t * SPW + s;
+        const bool valid = i < wend;
+        int rc = 0;
+        float A = 0.f;
+        if (valid) { rc = __ldg(a.rc + i); A = __ldg(a.amp + i); }
+        const int r = valid ? (rc >> 16) : rcur;
+        const int c = valid ? (rc & 0xffff) : 0;
+        if (r != rcur && r >= 0) {
+            if (FWD && rcur >= 0) flush(rcur);
+            if (BWD) {
+                const float4 *yr = Y + (int64_t)r * npv;
+                const float4 *cs = coef_s + g;
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                    float4 q = make_float4(0.f, 0.f, 0.f, 0.f), k4 = q;
+                    if (j < nv) { q = __ldg(yr + G * j); k4 = cs[G * j]; }
+                    vr[2 * j] = k4.x * q.x - k4.y * q.y;
+                    vi[2 * j] = k4.x * q.y + k4.y * q.x;
+                    vr[2 * j + 1] = k4.z * q.z - k4.w * q.w;
+                    vi[2 * j + 1] = k4.z * q.w + k4.w * q.z;
+                }
+            }
+            rcur = r;
+        }
+        float xr[NL], xi[NL];
+        const float4 *xc = X + (int64_t)c * npv;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (j < nv) q = __ldg(xc + G * j);
+            xr[2 * j] = q.x; xi[2 * j] = q.y; xr[2 * j + 1] = q.z; xi[2 * j + 1] = q.w;
+        }
+
+        float br, bi;
+        if (BWD) {
+            float s0r = 0.f, s0i = 0.f, s1r = 0.f, s1i = 0.f;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                s0r += vr[2 * j] * xr[2 * j] - vi[2 * j] * xi[2 * j];
+                s0i += vr[2 * j] * xi[2 * j] + vi[2 * j] * xr[2 * j];
+                s1r += vr[2 * j + 1] * xr[2 * j + 1] - vi[2 * j + 1] * xi[2 * j + 1];
+                s1i += vr[2 * j + 1] * xi[2 * j + 1] + vi[2 * j + 1] * xr[2 * j + 1];
+            }
+            float sr = s0r + s1r, si = s0i + s1i;
+            // Butterfly over the G lanes of the pixel (a+b == b+a: all lanes
+            // end with identical bits).
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) {
+                sr += __shfl_xor_sync(0xffffffffu, sr, o);
+                si += __shfl_xor_sync(0xffffffffu, si, o);
+            }
+            // b = A e^{-i arg S} = A conj(S)/|S|; arg(0) = 0 (kernels.py:115-119)
+            const float m2 = sr * sr + si * si;
+            if (m2 > 0.f && m2 < INFINITY) {
+                const float inv = rsqrtf(m2);
+                br = A * (sr * inv);
+                bi = -A * (si * inv);
+            } else if (sr != 0.f || si != 0.f) {
+                const float mx = fmaxf(fabsf(sr), fabsf(si));
+                const float xr_ = sr / mx, xi_ = si / mx;
+                const float inv = rsqrtf(xr_ * xr_ + xi_ * xi_);
+                br = A * (xr_ * inv);
+                bi = -A * (xi_ * inv);
+            } else {
+                br = A;
+                bi = 0.f;
+            }
+            if (WRITE && valid && g == 0) {
+                const int64_t di = a.dst ? (int64_t)a.dst[i] : i + a.idx_base;
+                if (di >= 0) {
+                    double ph = 0.0;
+                    if (sr != 0.f || si != 0.f) {
+                        ph = (double)atan2f(si, sr);
+                        if (ph >= kPi) ph -= kTwoPi;       // pi -> -pi convention
+                        else if (ph < -kPi) ph += kTwoPi;  // fp32 -pi lies below fp64 -pi
+                    }
+                    a.phase_out[(int64_t)pat * a.phase_stride + di] = ph;
+                }
+            }
+        } else {
+            double sn = 0.0, cs = 1.0;
+            if (valid) {
+                const int64_t di = a.dst ? (int64_t)a.dst[i] : i + a.idx_base;
+                if (di >= 0) sincos(a.phase_in[(int64_t)pat * a.phase_stride + di], &sn, &cs);
+            }
+            br = A * (float)cs;
+            bi = -A * (float)sn;
+        }
+
+        if (FWD) {
+#pragma unroll
+            for (int k = 0; k < NL; ++k) {
+                tr[k] += br * xr[k] - bi * xi[k];
+                ti[k] += br * xi[k] + bi * xr[k];
+            }
+        }
+    }
+
+    if (FWD) {
+        if (rcur >= 0) flush(rcur);
+        __syncthreads();
+        // per-chunk partial: slots folded in slot order (fixed)
+        const float2 *E2 = reinterpret_cast<const float2 *>(E_s);
+        float2 *out = a.partials + (int64_t)pat * a.part_stride + (int64_t)chunk * a.np;
+        for (int k = tid; k < a.np; k += kThreads) {
+            float sx = 0.f, sy = 0.f;
+            for (int q = 0; q < NSLOT; ++q) {
+                const float2 v = E2[q * a.np + k];
+                sx += v.x;
+                sy += v.y;
+            }
+            out[k] = make_float2(sx, sy);
+        }
+        if (a.u.act != ACT_NONE) {
+            __syncthreads();
+            hs_fold(a, pat, chunk, reinterpret_cast<char *>(E_s));
+        }
     }
 }
 

@@ -46,13 +46,14 @@ int fail(int code, const char *fmt, ...)
             return fail(HS_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(e_));  \
     } while (0)
 
-constexpr int kBlock = 64;  // spatial sort block (pixels) for pixel lists
+constexpr int kColBlock = 64;  // dense layout: columns per CTA chunk
 
 struct DevList {
     int32_t *rc = nullptr;
     float *amp = nullptr;
     int32_t *dst = nullptr;
     int64_t count = 0;
+    int32_t chunk_len = 0;  // 0: choose from kTargetChunks
 };
 
 template <typename T>
@@ -73,42 +74,41 @@ void dfree(T *&p)
     p = nullptr;
 }
 
+// G lanes per pixel, NLMAX spots per lane (template), nl active (even).
 struct Config {
-    int G, L, nl, np;
+    int G, NLMAX, nl, np, spw;
 };
 
 Config pick_config(int n)
 {
     Config c{};
-    if (n <= 16) { c.G = 1; c.L = 16; }
-    else if (n <= 32) { c.G = 2; c.L = 16; }
-    else if (n <= 64) { c.G = 4; c.L = 16; }
-    else if (n <= 128) { c.G = 8; c.L = 16; }
-    else if (n <= 256) { c.G = 16; c.L = 16; }
-    else if (n <= 512) { c.G = 32; c.L = 16; }
-    else { c.G = 32; c.L = 32; }
+    c.G = 1;
+    while (c.G < 32 && (n + c.G - 1) / c.G > 16) c.G *= 2;
+    c.NLMAX = ((n + c.G - 1) / c.G > 16) ? 32 : 16;
     c.nl = (n + c.G - 1) / c.G;
+    c.nl += c.nl & 1;
     c.np = c.G * c.nl;
+    c.spw = 32 / c.G;
     return c;
 }
 
 typedef void (*PassFn)(PassArgs);
 
-template <int G, int L>
+template <int G, int NL>
 PassFn pass_fn(int mode)
 {
     switch (mode) {
-    case PM_BWD | PM_WRITE: return hs_pass_kernel<G, L, PM_BWD | PM_WRITE>;
-    case PM_FWD: return hs_pass_kernel<G, L, PM_FWD>;
-    case PM_BWD | PM_FWD: return hs_pass_kernel<G, L, PM_BWD | PM_FWD>;
-    case PM_BWD | PM_FWD | PM_WRITE: return hs_pass_kernel<G, L, PM_BWD | PM_FWD | PM_WRITE>;
+    case PM_BWD | PM_WRITE: return hs_pass_kernel<G, NL, PM_BWD | PM_WRITE>;
+    case PM_FWD: return hs_pass_kernel<G, NL, PM_FWD>;
+    case PM_BWD | PM_FWD: return hs_pass_kernel<G, NL, PM_BWD | PM_FWD>;
+    case PM_BWD | PM_FWD | PM_WRITE: return hs_pass_kernel<G, NL, PM_BWD | PM_FWD | PM_WRITE>;
     default: return nullptr;
     }
 }
 
 PassFn select_pass(const Config &c, int mode)
 {
-    if (c.L == 32) return pass_fn<32, 32>(mode);
+    if (c.NLMAX == 32) return pass_fn<32, 32>(mode);
     switch (c.G) {
     case 1: return pass_fn<1, 16>(mode);
     case 2: return pass_fn<2, 16>(mode);
@@ -117,6 +117,11 @@ PassFn select_pass(const Config &c, int mode)
     case 16: return pass_fn<16, 16>(mode);
     default: return pass_fn<32, 16>(mode);
     }
+}
+
+size_t pass_smem(const Config &c)
+{
+    return (size_t)c.np * sizeof(float2) * (1 + kThreads / c.G);
 }
 
 }  // namespace
@@ -129,13 +134,16 @@ struct hs_plan {
     double c1 = 0, c2 = 0, sum_amp = 0;
     std::vector<int32_t> h_rows, h_cols;
     std::vector<float> h_amp;
+    std::vector<int32_t> h_index;  // grid -> storage index, -1 outside
+    std::vector<int32_t> row_lo, row_hi;
     double *d_axis = nullptr;
-    DevList storage;  // storage order, dst = nullptr
-    DevList dense;    // block-sorted, dst = storage index
-    std::map<std::pair<int64_t, int64_t>, DevList> windows;
+    DevList storage;                      // storage order
+    std::map<int, DevList> dense;         // full range, banded layout per slots-per-warp
+    std::map<std::pair<int64_t, int64_t>, DevList> windows;  // sorted (row, col)
 
     // spot batch
     int batch = 0, n = 0, cap_batch = 0, cap_np = 0;
+    int64_t cap_chunks = 0;
     Config cfg{};
     bool tables_valid = false;
     double *d_x = nullptr, *d_y = nullptr, *d_z = nullptr, *d_a0 = nullptr;
@@ -144,60 +152,36 @@ struct hs_plan {
     double *d_w = nullptr;
     float2 *d_coef = nullptr;
     float2 *d_part = nullptr;
-    int64_t part_stride = 0;
+    double2 *d_gpart = nullptr;
+    int32_t *d_grp_cnt = nullptr, *d_pat_cnt = nullptr;
+    int64_t part_stride = 0, gpart_stride = 0;
+    int32_t cnt_stride = 0;
     int32_t *d_status = nullptr, *d_degen = nullptr, *d_qstatus = nullptr;
     double *d_fields = nullptr, *d_e = nullptr, *d_u = nullptr, *d_inten = nullptr, *d_rel = nullptr;
-    double *d_phase = nullptr;   // [cap_batch][m] solver output / API scratch
+    double *d_phase = nullptr;   // [cap_batch][m]
     double *d_trace_w = nullptr, *d_trace_m = nullptr;
     int64_t trace_cap = 0;
 
-    // last solve
     int last_alg = -1, last_iters = 0, last_flags = 0;
     int64_t last_launches = 0;
-
-    // graph cache
     std::map<std::tuple<int, int, int64_t, int, int, int>, cudaGraphExec_t> graphs;
-
-    int launches = 0;  // counter while recording
 };
 
 namespace {
 
-void sort_list(const hs_plan *p, std::vector<int64_t> &idx)
+int upload_entries(const std::vector<int32_t> &rc, const std::vector<float> &amp,
+                   const std::vector<int32_t> *dst, int32_t chunk_len, DevList *out)
 {
-    const int nb = (p->side + kBlock - 1) / kBlock;
-    std::vector<std::pair<int64_t, int64_t>> keyed(idx.size());
-    for (size_t i = 0; i < idx.size(); ++i) {
-        const int64_t s = idx[i];
-        const int64_t r = p->h_rows[s], c = p->h_cols[s];
-        const int64_t key = ((r / kBlock) * nb + c / kBlock) * (int64_t)(kBlock * kBlock) +
-                            (r % kBlock) * kBlock + (c % kBlock);
-        keyed[i] = {key, s};
-    }
-    std::sort(keyed.begin(), keyed.end());
-    for (size_t i = 0; i < idx.size(); ++i) idx[i] = keyed[i].second;
-}
-
-int upload_list(const hs_plan *p, const std::vector<int64_t> &idx, bool with_dst, DevList *out)
-{
-    const int64_t cnt = (int64_t)idx.size();
-    std::vector<int32_t> rc(cnt), dst(with_dst ? cnt : 0);
-    std::vector<float> amp(cnt);
-    for (int64_t i = 0; i < cnt; ++i) {
-        const int64_t s = idx[i];
-        rc[i] = (p->h_rows[s] << 16) | p->h_cols[s];
-        amp[i] = p->h_amp[s];
-        if (with_dst) dst[i] = (int32_t)s;
-    }
-    int rcode;
-    if ((rcode = dalloc(&out->rc, cnt)) || (rcode = dalloc(&out->amp, cnt))) return rcode;
-    if (with_dst && (rcode = dalloc(&out->dst, cnt))) return rcode;
+    const int64_t cnt = (int64_t)rc.size();
+    int r;
+    if ((r = dalloc(&out->rc, cnt)) || (r = dalloc(&out->amp, cnt))) return r;
+    if (dst && (r = dalloc(&out->dst, cnt))) return r;
     out->count = cnt;
+    out->chunk_len = chunk_len;
     if (cnt) {
         CUDA_TRY(cudaMemcpy(out->rc, rc.data(), cnt * sizeof(int32_t), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(out->amp, amp.data(), cnt * sizeof(float), cudaMemcpyHostToDevice));
-        if (with_dst)
-            CUDA_TRY(cudaMemcpy(out->dst, dst.data(), cnt * sizeof(int32_t), cudaMemcpyHostToDevice));
+        if (dst) CUDA_TRY(cudaMemcpy(out->dst, dst->data(), cnt * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     return HS_OK;
 }
@@ -210,25 +194,108 @@ void free_list(DevList &l)
     l.count = 0;
 }
 
-int get_window(hs_plan *p, int64_t start, int64_t count, const DevList **out)
+inline int32_t pack_rc(int r, int c) { return (r << 16) | c; }
+
+// Storage-order list: entry i is storage pixel i (API ranges slice it).
+int build_storage(hs_plan *p)
 {
-    if (start == 0 && count == p->m) {
-        *out = &p->dense;
+    std::vector<int32_t> rc(p->m);
+    for (int64_t i = 0; i < p->m; ++i) rc[i] = pack_rc(p->h_rows[i], p->h_cols[i]);
+    return upload_entries(rc, p->h_amp, nullptr, 0, &p->storage);
+}
+
+// Full-range list for `spw` slots per warp: bands of 8*Rw rows split into
+// blocks of kColBlock columns (one CTA chunk each); inside a block warp w owns
+// rows band+w*Rw .. +Rw, and each warp step covers Rw rows x Cw columns, slot s
+// at (row s % Rw, column s / Rw).  Off-aperture cells are zero-amplitude
+// padding (dst = -1).
+int get_dense(hs_plan *p, int spw, const DevList **out)
+{
+    auto it = p->dense.find(spw);
+    if (it != p->dense.end()) {
+        *out = &it->second;
         return HS_OK;
     }
+    const int Rw = std::min(spw, 4), Cw = spw / Rw, TB = kWarps * Rw;
+    std::vector<int32_t> rc, dst;
+    std::vector<float> amp;
+    const int side = p->side;
+    for (int b0 = 0; b0 < side; b0 += TB) {
+        int lo = side, hi = 0;
+        for (int r = b0; r < std::min(b0 + TB, side); ++r) {
+            lo = std::min(lo, p->row_lo[r]);
+            hi = std::max(hi, p->row_hi[r]);
+        }
+        if (hi <= lo) continue;
+        const int nblk = (hi - lo + kColBlock - 1) / kColBlock;
+        for (int blk = 0; blk < nblk; ++blk) {
+            const int c0 = lo + blk * kColBlock;
+            for (int w = 0; w < kWarps; ++w)
+                for (int t = 0; t < kColBlock / Cw; ++t)
+                    for (int s = 0; s < spw; ++s) {
+                        const int row = b0 + w * Rw + s % Rw;
+                        const int col = c0 + t * Cw + s / Rw;
+                        int32_t idx = -1;
+                        if (row < side && col < side) idx = p->h_index[(int64_t)row * side + col];
+                        rc.push_back(pack_rc(std::min(row, side - 1), std::min(col, side - 1)));
+                        amp.push_back(idx >= 0 ? p->h_amp[idx] : 0.f);
+                        dst.push_back(idx);
+                    }
+        }
+    }
+    DevList l;
+    int r = upload_entries(rc, amp, &dst, TB * kColBlock, &l);
+    if (r) return r;
+    it = p->dense.emplace(spw, l).first;
+    *out = &it->second;
+    return HS_OK;
+}
+
+// Compressed window: storage range [start, start+count) sorted by (row, col).
+int get_window(hs_plan *p, int64_t start, int64_t count, const DevList **out)
+{
     auto key = std::make_pair(start, count);
     auto it = p->windows.find(key);
     if (it == p->windows.end()) {
-        std::vector<int64_t> idx(count);
-        for (int64_t i = 0; i < count; ++i) idx[i] = start + i;
-        sort_list(p, idx);
+        std::vector<int64_t> keyed(count);
+        for (int64_t i = 0; i < count; ++i) {
+            const int64_t s = start + i;
+            keyed[i] = ((int64_t)p->h_rows[s] * p->side + p->h_cols[s]) * p->m + s;
+        }
+        std::sort(keyed.begin(), keyed.end());
+        std::vector<int32_t> rc(count);
+        std::vector<float> amp(count);
+        for (int64_t i = 0; i < count; ++i) {
+            const int64_t s = keyed[i] % p->m;
+            rc[i] = pack_rc(p->h_rows[s], p->h_cols[s]);
+            amp[i] = p->h_amp[s];
+        }
         DevList l;
-        int rc = upload_list(p, idx, false, &l);
-        if (rc) return rc;
+        int r = upload_entries(rc, amp, nullptr, 0, &l);
+        if (r) return r;
         it = p->windows.emplace(key, l).first;
     }
     *out = &it->second;
     return HS_OK;
+}
+
+struct Geom {
+    int32_t chunk_len, nchunks;
+};
+
+Geom geom_of(const DevList &l, int64_t count, int spw)
+{
+    Geom g;
+    if (l.chunk_len) {
+        g.chunk_len = l.chunk_len;
+    } else {
+        const int64_t unit = (int64_t)kWarps * spw;
+        int64_t per = (count + kTargetChunks - 1) / kTargetChunks;
+        per = ((per + unit - 1) / unit) * unit;
+        g.chunk_len = (int32_t)std::max<int64_t>(per, unit);
+    }
+    g.nchunks = (int32_t)((count + g.chunk_len - 1) / g.chunk_len);
+    return g;
 }
 
 void free_graphs(hs_plan *p)
@@ -237,15 +304,25 @@ void free_graphs(hs_plan *p)
     p->graphs.clear();
 }
 
+void free_fold(hs_plan *p)
+{
+    dfree(p->d_part);
+    dfree(p->d_gpart);
+    dfree(p->d_grp_cnt);
+    dfree(p->d_pat_cnt);
+    p->cap_chunks = 0;
+}
+
 void free_batch(hs_plan *p)
 {
     dfree(p->d_x); dfree(p->d_y); dfree(p->d_z); dfree(p->d_a0);
     dfree(p->d_theta); dfree(p->d_amp_in);
-    dfree(p->d_gx); dfree(p->d_gy); dfree(p->d_w); dfree(p->d_coef); dfree(p->d_part);
+    dfree(p->d_gx); dfree(p->d_gy); dfree(p->d_w); dfree(p->d_coef);
     dfree(p->d_status); dfree(p->d_degen); dfree(p->d_qstatus);
     dfree(p->d_fields); dfree(p->d_e); dfree(p->d_u); dfree(p->d_inten); dfree(p->d_rel);
     dfree(p->d_phase);
     dfree(p->d_trace_w); dfree(p->d_trace_m);
+    free_fold(p);
     p->cap_batch = p->cap_np = 0;
     p->trace_cap = 0;
     free_graphs(p);
@@ -254,28 +331,47 @@ void free_batch(hs_plan *p)
 int ensure_batch(hs_plan *p, int batch, int n)
 {
     const Config cfg = pick_config(n);
-    if (batch <= p->cap_batch && cfg.np <= p->cap_np && n <= p->cap_np) return HS_OK;
+    if (batch <= p->cap_batch && cfg.np <= p->cap_np) return HS_OK;
     free_batch(p);
     const int B = batch;
-    const int np = cfg.np;
-    const size_t bn = (size_t)B * np;
-    p->part_stride = (int64_t)(kTargetChunks + 8) * np;
+    const size_t bn = (size_t)B * cfg.np;
     int rc;
     if ((rc = dalloc(&p->d_x, bn)) || (rc = dalloc(&p->d_y, bn)) || (rc = dalloc(&p->d_z, bn)) ||
-        (rc = dalloc(&p->d_a0, bn)) || (rc = dalloc(&p->d_theta, bn)) ||
-        (rc = dalloc(&p->d_amp_in, bn)) ||
-        (rc = dalloc(&p->d_gx, (size_t)B * p->side * np)) ||
-        (rc = dalloc(&p->d_gy, (size_t)B * p->side * np)) || (rc = dalloc(&p->d_w, bn)) ||
-        (rc = dalloc(&p->d_coef, bn)) || (rc = dalloc(&p->d_part, (size_t)B * p->part_stride)) ||
-        (rc = dalloc(&p->d_status, B)) || (rc = dalloc(&p->d_degen, B)) ||
-        (rc = dalloc(&p->d_qstatus, B)) || (rc = dalloc(&p->d_fields, bn * 2)) ||
-        (rc = dalloc(&p->d_e, B)) || (rc = dalloc(&p->d_u, B)) || (rc = dalloc(&p->d_inten, bn)) ||
-        (rc = dalloc(&p->d_rel, bn)) || (rc = dalloc(&p->d_phase, (size_t)B * p->m))) {
+        (rc = dalloc(&p->d_a0, bn)) || (rc = dalloc(&p->d_theta, bn)) || (rc = dalloc(&p->d_amp_in, bn)) ||
+        (rc = dalloc(&p->d_gx, (size_t)B * p->side * cfg.np)) ||
+        (rc = dalloc(&p->d_gy, (size_t)B * p->side * cfg.np)) || (rc = dalloc(&p->d_w, bn)) ||
+        (rc = dalloc(&p->d_coef, bn)) || (rc = dalloc(&p->d_status, B)) || (rc = dalloc(&p->d_degen, B)) ||
+        (rc = dalloc(&p->d_qstatus, B)) || (rc = dalloc(&p->d_fields, bn * 2)) || (rc = dalloc(&p->d_e, B)) ||
+        (rc = dalloc(&p->d_u, B)) || (rc = dalloc(&p->d_inten, bn)) || (rc = dalloc(&p->d_rel, bn)) ||
+        (rc = dalloc(&p->d_phase, (size_t)B * p->m))) {
         free_batch(p);
         return rc;
     }
+    CUDA_TRY(cudaMemset(p->d_status, 0, sizeof(int32_t) * B));
     p->cap_batch = B;
-    p->cap_np = np;
+    p->cap_np = cfg.np;
+    return HS_OK;
+}
+
+// Fold buffers sized for `chunks` partials per pattern.
+int ensure_fold(hs_plan *p, int64_t chunks)
+{
+    if (chunks <= p->cap_chunks && p->d_part) return HS_OK;
+    free_fold(p);
+    free_graphs(p);
+    const int64_t groups = (chunks + kGroup - 1) / kGroup;
+    const int B = p->cap_batch, np = p->cap_np;
+    p->part_stride = chunks * np;
+    p->gpart_stride = groups * np;
+    p->cnt_stride = (int32_t)groups;
+    int rc;
+    if ((rc = dalloc(&p->d_part, (size_t)B * p->part_stride)) ||
+        (rc = dalloc(&p->d_gpart, (size_t)B * p->gpart_stride)) ||
+        (rc = dalloc(&p->d_grp_cnt, (size_t)B * groups)) || (rc = dalloc(&p->d_pat_cnt, (size_t)B)))
+        return rc;
+    CUDA_TRY(cudaMemset(p->d_grp_cnt, 0, sizeof(int32_t) * B * groups));
+    CUDA_TRY(cudaMemset(p->d_pat_cnt, 0, sizeof(int32_t) * B));
+    p->cap_chunks = chunks;
     return HS_OK;
 }
 
@@ -288,93 +384,23 @@ int ensure_trace(hs_plan *p, int iters)
     int rc;
     if ((rc = dalloc(&p->d_trace_w, need)) || (rc = dalloc(&p->d_trace_m, need))) return rc;
     p->trace_cap = need;
-    free_graphs(p);  // graphs bake the trace pointers
+    free_graphs(p);
     return HS_OK;
 }
 
-// ---- launch helpers (record into the current stream / capture) ----------
-
-struct PassGeom {
-    int32_t chunk_len;
-    int32_t nchunks;
-};
-
-PassGeom pass_geom(int64_t count, int G)
-{
-    const int nslots = kThreads / G;
-    int64_t per = (count + kTargetChunks - 1) / kTargetChunks;
-    per = ((per + nslots - 1) / nslots) * nslots;
-    if (per < nslots) per = nslots;
-    PassGeom g;
-    g.chunk_len = (int32_t)per;
-    g.nchunks = (int32_t)((count + per - 1) / per);
-    return g;
-}
-
-int launch_tables(hs_plan *p)
-{
-    dim3 grid(p->side, p->batch);
-    hs_tables_kernel<<<grid, 128, 0, p->stream>>>(p->side, p->cfg.np, p->n, p->d_axis, p->c1, p->c2,
-                                                  p->d_x, p->d_y, p->d_z, p->d_gx, p->d_gy);
-    p->launches++;
-    CUDA_TRY(cudaGetLastError());
-    return HS_OK;
-}
-
-// Launch one pass over `list` (+offset) for all patterns; returns nchunks.
-int launch_pass(hs_plan *p, int mode, const int32_t *rc, const float *amp, const int32_t *dst,
-                int64_t idx_base, int64_t count, const double *phase_in, double *phase_out,
-                int64_t phase_stride, int32_t *nchunks_out)
-{
-    const Config &c = p->cfg;
-    PassGeom geo = pass_geom(count, c.G);
-    *nchunks_out = geo.nchunks;
-    if (count == 0) return HS_OK;
-    PassArgs a;
-    a.rc = rc;
-    a.amp = amp;
-    a.dst = dst;
-    a.idx_base = idx_base;
-    a.count = count;
-    a.chunk_len = geo.chunk_len;
-    a.side = p->side;
-    a.np = c.np;
-    a.tab_stride = (int64_t)p->side * c.np;
-    a.gx = p->d_gx;
-    a.gy = p->d_gy;
-    a.coef = p->d_coef;
-    a.phase_in = phase_in;
-    a.phase_out = phase_out;
-    a.phase_stride = phase_stride;
-    a.partials = p->d_part;
-    a.part_stride = p->part_stride;
-    a.status = p->d_status;
-    PassFn fn = select_pass(c, mode);
-    const size_t smem = (mode & PM_FWD) ? (size_t)(kThreads / c.G) * c.np * sizeof(float2) : 0;
-    dim3 grid(geo.nchunks, p->batch);
-    fn<<<grid, kThreads, smem, p->stream>>>(a);
-    p->launches++;
-    CUDA_TRY(cudaGetLastError());
-    return HS_OK;
-}
-
-UpdArgs upd_args(hs_plan *p, int mode, int nchunks)
+UpdArgs upd_args(hs_plan *p, int act)
 {
     UpdArgs u;
     memset(&u, 0, sizeof u);
-    u.mode = mode;
+    u.act = act;
     u.n = p->n;
     u.np = p->cfg.np;
-    u.nchunks = nchunks;
-    u.partials = p->d_part;
-    u.part_stride = p->part_stride;
-    u.amp_in = p->d_amp_in;
-    u.theta_in = p->d_theta;
     u.a0 = p->d_a0;
     u.w = p->d_w;
     u.coef = p->d_coef;
     u.trace_w = p->d_trace_w;
     u.trace_m = p->d_trace_m;
+    u.iters = 1;
     u.status = p->d_status;
     u.degen = p->d_degen;
     u.qstatus = p->d_qstatus;
@@ -387,10 +413,53 @@ UpdArgs upd_args(hs_plan *p, int mode, int nchunks)
     return u;
 }
 
-int launch_update(hs_plan *p, const UpdArgs &u)
+int launch_tables(hs_plan *p, bool seed)
 {
-    hs_update_kernel<<<p->batch, kUpdThreads, 0, p->stream>>>(u);
-    p->launches++;
+    dim3 grid(p->side, p->batch);
+    hs_tables_kernel<<<grid, 128, 0, p->stream>>>(p->side, p->cfg.np, p->n, p->d_axis, p->c1, p->c2, p->d_x,
+                                                  p->d_y, p->d_z, p->d_gx, p->d_gy, p->d_a0,
+                                                  seed ? p->d_theta : nullptr, p->d_coef, p->d_w);
+    CUDA_TRY(cudaGetLastError());
+    return HS_OK;
+}
+
+// One pass over `count` entries of list `l` starting at entry `off`.
+int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t count, int64_t idx_base,
+                const double *phase_in, double *phase_out, int64_t phase_stride, const UpdArgs &u)
+{
+    const Config &c = p->cfg;
+    const Geom geo = geom_of(l, count, c.spw);
+    if (count == 0) return HS_OK;
+    if (geo.nchunks > p->cap_chunks) return fail(HS_ECUDA, "fold buffers too small (%d chunks)", geo.nchunks);
+    PassArgs a;
+    memset(&a, 0, sizeof a);
+    a.rc = l.rc + off;
+    a.amp = l.amp + off;
+    a.dst = l.dst ? l.dst + off : nullptr;
+    a.idx_base = idx_base;
+    a.count = count;
+    a.chunk_len = geo.chunk_len;
+    a.nchunks = geo.nchunks;
+    a.np = c.np;
+    a.nl = c.nl;
+    a.tab_stride = (int64_t)p->side * c.np;
+    a.gx = p->d_gx;
+    a.gy = p->d_gy;
+    a.coef = p->d_coef;
+    a.phase_in = phase_in;
+    a.phase_out = phase_out;
+    a.phase_stride = phase_stride;
+    a.partials = p->d_part;
+    a.part_stride = p->part_stride;
+    a.gpart = p->d_gpart;
+    a.gpart_stride = p->gpart_stride;
+    a.grp_cnt = p->d_grp_cnt;
+    a.pat_cnt = p->d_pat_cnt;
+    a.cnt_stride = p->cnt_stride;
+    a.u = u;
+    PassFn fn = select_pass(c, mode);
+    dim3 grid(geo.nchunks, p->batch);
+    fn<<<grid, kThreads, pass_smem(c), p->stream>>>(a);
     CUDA_TRY(cudaGetLastError());
     return HS_OK;
 }
@@ -406,75 +475,48 @@ int reset_status(hs_plan *p)
 int ensure_tables(hs_plan *p)
 {
     if (p->tables_valid) return HS_OK;
-    int rc = launch_tables(p);
+    int rc = launch_tables(p, false);
     if (rc) return rc;
     p->tables_valid = true;
     return HS_OK;
 }
 
-// The solve schedule (solvers.py:192-235), fused:
-//   pass_0 = superpose(coef_0) + forward over read_1
-//   for j = 1..I: update_j (forward fields of pass_{j-1} -> coef_j);
-//                 pass_j = superpose(coef_j) over write_j + forward over write_j
-//                 (= read_{j+1}); the last pass writes the phase and yields
-//                 the full-range fields of quality_report.
+// The solve schedule (solvers.py:192-235), fused: pass 0 superposes coef_0
+// over read_1 and projects it; the fold of pass j applies iteration j+1's
+// update (trace record j+1, coef_{j+1}); pass j >= 1 superposes coef_j over
+// write_j (= read_{j+1}); the last pass writes the phase and yields the
+// full-range fields of quality_report.
 int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags)
 {
     int rc;
     const bool want_fields = (flags & HS_WANT_FIELDS) != 0;
-    if ((rc = reset_status(p))) return rc;
-    if ((rc = launch_tables(p))) return rc;
-    UpdArgs seed = upd_args(p, UPD_SEED, 0);
-    seed.amp_in = p->d_a0;
-    if ((rc = launch_update(p, seed))) return rc;
-    int32_t nch = 0;
     const int64_t m = p->m;
-    if (alg == HS_ALG_RS) {
-        const int mode = want_fields ? (PM_BWD | PM_FWD | PM_WRITE) : (PM_BWD | PM_WRITE);
-        if ((rc = launch_pass(p, mode, p->dense.rc, p->dense.amp, p->dense.dst, 0, m, nullptr,
-                              p->d_phase, m, &nch)))
-            return rc;
-        if (want_fields && (rc = launch_update(p, upd_args(p, UPD_FINAL, nch)))) return rc;
-        return HS_OK;
-    }
+    if ((rc = reset_status(p))) return rc;
+    if ((rc = launch_tables(p, true))) return rc;
+    const DevList *dense;
+    if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
+    const int final_mode = want_fields ? (PM_BWD | PM_FWD | PM_WRITE) : (PM_BWD | PM_WRITE);
+    const UpdArgs fin = upd_args(p, want_fields ? ACT_FINAL : ACT_NONE);
+    if (alg == HS_ALG_RS)
+        return launch_pass(p, final_mode, *dense, 0, dense->count, 0, nullptr, p->d_phase, m, fin);
     const int cs = (subset < m) ? std::max(0, iters - 2) : 0;
     const int64_t half = std::max<int64_t>(1, subset / 2);
-    // window written by iteration j (1-based), j <= cs
-    auto window_of = [&](int j, const DevList **l) -> int {
-        const int64_t off = ((int64_t)(j - 1) * half) % (m - subset + 1);
-        return get_window(p, off, subset, l);
-    };
-    const DevList *lst = nullptr;
-    if (cs > 0) {
-        if ((rc = get_window(p, 0, subset, &lst))) return rc;
-    } else {
-        lst = &p->dense;
-    }
-    if ((rc = launch_pass(p, PM_BWD | PM_FWD, lst->rc, lst->amp, nullptr, 0, lst->count, nullptr,
-                          nullptr, 0, &nch)))
-        return rc;
-    for (int j = 1; j <= iters; ++j) {
-        UpdArgs u = upd_args(p, UPD_STEP, nch);
-        u.iter = j - 1;
-        u.iters = iters;
-        if ((rc = launch_update(p, u))) return rc;
-        const bool last = (j == iters);
-        if (j <= cs) {
-            if ((rc = window_of(j, &lst))) return rc;
-        } else {
-            lst = &p->dense;
+    for (int j = 0; j <= iters; ++j) {
+        // list of pass j: read_1 for j = 0, write_j otherwise
+        const DevList *lst = dense;
+        if (j == 0 ? cs > 0 : j <= cs) {
+            const int64_t off = (j == 0) ? 0 : ((int64_t)(j - 1) * half) % (m - subset + 1);
+            if ((rc = get_window(p, off, subset, &lst))) return rc;
         }
-        if (last) {
-            const int mode = want_fields ? (PM_BWD | PM_FWD | PM_WRITE) : (PM_BWD | PM_WRITE);
-            if ((rc = launch_pass(p, mode, lst->rc, lst->amp, lst->dst, 0, lst->count, nullptr,
-                                  p->d_phase, m, &nch)))
-                return rc;
-            if (want_fields && (rc = launch_update(p, upd_args(p, UPD_FINAL, nch)))) return rc;
+        if (j < iters) {
+            UpdArgs u = upd_args(p, ACT_STEP);
+            u.iter = j;
+            u.iters = iters;
+            rc = launch_pass(p, PM_BWD | PM_FWD, *lst, 0, lst->count, 0, nullptr, nullptr, 0, u);
         } else {
-            if ((rc = launch_pass(p, PM_BWD | PM_FWD, lst->rc, lst->amp, nullptr, 0, lst->count,
-                                  nullptr, nullptr, 0, &nch)))
-                return rc;
+            rc = launch_pass(p, final_mode, *lst, 0, lst->count, 0, nullptr, p->d_phase, m, fin);
         }
+        if (rc) return rc;
     }
     return HS_OK;
 }
@@ -502,8 +544,7 @@ const char *hs_last_error(void) { return g_err.c_str(); }
 int hs_device_count(int *count)
 {
     int n = 0;
-    cudaError_t e = cudaGetDeviceCount(&n);
-    if (e != cudaSuccess) {
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
         cudaGetLastError();
         n = 0;
     }
@@ -518,9 +559,8 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
                    double sum_amplitude, hs_plan **out)
 {
     *out = nullptr;
-    if (side < 2 || side > 65535) return fail(HS_EINVAL, "side_px %d outside 2..65535", side);
+    if (side < 2 || side > 32767) return fail(HS_EINVAL, "side_px %d outside 2..32767", side);
     if (m < 1 || m > (int64_t)side * side) return fail(HS_EINVAL, "pixel count %lld invalid", (long long)m);
-    if (m > INT32_MAX) return fail(HS_EINVAL, "pixel count too large");
     std::unique_ptr<hs_plan> p(new hs_plan);
     p->device = device;
     CUDA_TRY(cudaSetDevice(device));
@@ -533,27 +573,30 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
     p->h_rows.resize(m);
     p->h_cols.resize(m);
     p->h_amp.resize(m);
+    p->h_index.assign((size_t)side * side, -1);
+    p->row_lo.assign(side, side);
+    p->row_hi.assign(side, 0);
     for (int64_t i = 0; i < m; ++i) {
         if (rows[i] < 0 || rows[i] >= side || cols[i] < 0 || cols[i] >= side)
             return fail(HS_EINVAL, "pixel %lld outside the grid", (long long)i);
-        p->h_rows[i] = (int32_t)rows[i];
-        p->h_cols[i] = (int32_t)cols[i];
+        const int r = (int)rows[i], c = (int)cols[i];
+        if (p->h_index[(size_t)r * side + c] >= 0) return fail(HS_EINVAL, "duplicate pixel (%d, %d)", r, c);
+        p->h_rows[i] = r;
+        p->h_cols[i] = c;
         p->h_amp[i] = (float)amplitude[i];
+        p->h_index[(size_t)r * side + c] = (int32_t)i;
+        p->row_lo[r] = std::min(p->row_lo[r], c);
+        p->row_hi[r] = std::max(p->row_hi[r], c + 1);
     }
     int rc;
     if ((rc = dalloc(&p->d_axis, side))) return rc;
     CUDA_TRY(cudaMemcpy(p->d_axis, axis, sizeof(double) * side, cudaMemcpyHostToDevice));
-    std::vector<int64_t> idx(m);
-    for (int64_t i = 0; i < m; ++i) idx[i] = i;
-    if ((rc = upload_list(p.get(), idx, false, &p->storage))) return rc;
-    sort_list(p.get(), idx);
-    if ((rc = upload_list(p.get(), idx, true, &p->dense))) return rc;
-    // 64 KB dynamic shared memory for the widest pass variant.
+    if ((rc = build_storage(p.get()))) return rc;
     const int modes[4] = {PM_BWD | PM_WRITE, PM_FWD, PM_BWD | PM_FWD, PM_BWD | PM_FWD | PM_WRITE};
     for (int mode : modes) {
-        Config c{32, 32, 32, 1024};
+        Config c{32, 32, 32, 1024, 1};
         CUDA_TRY(cudaFuncSetAttribute(select_pass(c, mode), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      65536));
+                                      (int)pass_smem(c)));
     }
     *out = p.release();
     return HS_OK;
@@ -566,7 +609,7 @@ void hs_plan_destroy(hs_plan *p)
     cudaStreamSynchronize(p->stream);
     free_batch(p);
     free_list(p->storage);
-    free_list(p->dense);
+    for (auto &kv : p->dense) free_list(kv.second);
     for (auto &kv : p->windows) free_list(kv.second);
     dfree(p->d_axis);
     cudaStreamDestroy(p->stream);
@@ -585,6 +628,10 @@ int hs_set_spots(hs_plan *p, int batch, int n, const double *x, const double *y,
     p->batch = batch;
     p->n = n;
     p->cfg = pick_config(n);
+    const DevList *dense;
+    if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
+    const int64_t chunks = std::max<int64_t>(geom_of(*dense, dense->count, p->cfg.spw).nchunks, kTargetChunks + 1);
+    if ((rc = ensure_fold(p, chunks))) return rc;
     const size_t bytes = sizeof(double) * (size_t)batch * n;
     CUDA_TRY(cudaMemcpyAsync(p->d_x, x, bytes, cudaMemcpyHostToDevice, p->stream));
     CUDA_TRY(cudaMemcpyAsync(p->d_y, y, bytes, cudaMemcpyHostToDevice, p->stream));
@@ -594,88 +641,93 @@ int hs_set_spots(hs_plan *p, int batch, int n, const double *x, const double *y,
     return HS_OK;
 }
 
+static int check_range(hs_plan *p, int64_t start, int64_t stop)
+{
+    if (p->batch < 1) return fail(HS_EINVAL, "no spots set");
+    if (start < 0 || start > stop || stop > p->m)
+        return fail(HS_EINVAL, "pixel range (%lld, %lld) outside 0..%lld", (long long)start, (long long)stop,
+                    (long long)p->m);
+    return HS_OK;
+}
+
+// API passes act on pattern 0 only.
+struct OnePattern {
+    hs_plan *p;
+    int saved;
+    explicit OnePattern(hs_plan *pl) : p(pl), saved(pl->batch) { p->batch = 1; }
+    ~OnePattern() { p->batch = saved; }
+};
+
 int hs_superpose(hs_plan *p, const double *amplitude, const double *theta, int64_t start, int64_t stop,
                  double *out)
 {
-    if (p->batch < 1) return fail(HS_EINVAL, "no spots set");
-    if (start < 0 || start > stop || stop > p->m)
-        return fail(HS_EINVAL, "pixel range (%lld, %lld) outside 0..%lld", (long long)start,
-                    (long long)stop, (long long)p->m);
     int rc;
-    if ((rc = check_device(p)) || (rc = ensure_tables(p)) || (rc = reset_status(p))) return rc;
+    if ((rc = check_range(p, start, stop)) || (rc = check_device(p)) || (rc = ensure_tables(p)) ||
+        (rc = reset_status(p)))
+        return rc;
+    if (stop == start) return HS_OK;
     const size_t bytes = sizeof(double) * p->n;
     CUDA_TRY(cudaMemcpyAsync(p->d_amp_in, amplitude, bytes, cudaMemcpyHostToDevice, p->stream));
     CUDA_TRY(cudaMemcpyAsync(p->d_theta, theta, bytes, cudaMemcpyHostToDevice, p->stream));
-    const int saved = p->batch;
-    p->batch = 1;
-    UpdArgs seed = upd_args(p, UPD_SEED, 0);
-    seed.w = nullptr;
-    rc = launch_update(p, seed);
-    int32_t nch;
-    if (!rc)
-        rc = launch_pass(p, PM_BWD | PM_WRITE, p->storage.rc + start, p->storage.amp + start, nullptr, 0,
-                         stop - start, nullptr, p->d_phase, 0, &nch);
-    p->batch = saved;
-    if (rc) return rc;
-    if (stop > start)
-        CUDA_TRY(cudaMemcpyAsync(out, p->d_phase, sizeof(double) * (stop - start), cudaMemcpyDeviceToHost,
-                                 p->stream));
-    return sync_and_check(p);
-}
-
-static int forward_common(hs_plan *p, const double *phase, int64_t start, int64_t stop, int mode)
-{
-    if (p->batch < 1) return fail(HS_EINVAL, "no spots set");
-    if (start < 0 || start > stop || stop > p->m)
-        return fail(HS_EINVAL, "pixel range (%lld, %lld) outside 0..%lld", (long long)start,
-                    (long long)stop, (long long)p->m);
-    int rc;
-    if ((rc = check_device(p)) || (rc = ensure_tables(p)) || (rc = reset_status(p))) return rc;
-    CUDA_TRY(cudaMemcpyAsync(p->d_phase, phase, sizeof(double) * p->m, cudaMemcpyHostToDevice, p->stream));
-    const int saved = p->batch;
-    p->batch = 1;
-    int32_t nch = 0;
-    if (stop > start) {
-        rc = launch_pass(p, PM_FWD, p->storage.rc + start, p->storage.amp + start, nullptr, start,
-                         stop - start, p->d_phase, nullptr, 0, &nch);
-    } else {
-        // empty range: zero fields (kernels.py:234-235) via a zero partial
-        cudaMemsetAsync(p->d_part, 0, sizeof(float2) * p->cfg.np, p->stream);
-        nch = 1;
+    {
+        OnePattern one(p);
+        hs_seed_kernel<<<1, 256, 0, p->stream>>>(p->n, p->cfg.np, p->d_amp_in, p->d_theta, p->d_coef, nullptr);
+        CUDA_TRY(cudaGetLastError());
+        rc = launch_pass(p, PM_BWD | PM_WRITE, p->storage, start, stop - start, 0, nullptr, p->d_phase, 0,
+                         upd_args(p, ACT_NONE));
+        if (rc) return rc;
     }
-    if (!rc) rc = launch_update(p, upd_args(p, mode, nch));
-    p->batch = saved;
-    return rc;
+    CUDA_TRY(cudaMemcpyAsync(out, p->d_phase, sizeof(double) * (stop - start), cudaMemcpyDeviceToHost, p->stream));
+    return sync_and_check(p);
 }
 
 int hs_forward(hs_plan *p, const double *phase, int64_t start, int64_t stop, double *fields)
 {
-    int rc = forward_common(p, phase, start, stop, UPD_FIELDS);
-    if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(fields, p->d_fields, sizeof(double) * 2 * p->n, cudaMemcpyDeviceToHost,
-                             p->stream));
+    int rc;
+    if ((rc = check_range(p, start, stop)) || (rc = check_device(p)) || (rc = ensure_tables(p)) ||
+        (rc = reset_status(p)))
+        return rc;
+    if (stop == start) {  // kernels.py:234-235
+        memset(fields, 0, sizeof(double) * 2 * p->n);
+        return HS_OK;
+    }
+    CUDA_TRY(cudaMemcpyAsync(p->d_phase, phase, sizeof(double) * p->m, cudaMemcpyHostToDevice, p->stream));
+    {
+        OnePattern one(p);
+        rc = launch_pass(p, PM_FWD, p->storage, start, stop - start, start, p->d_phase, nullptr, 0,
+                         upd_args(p, ACT_FIELDS));
+        if (rc) return rc;
+    }
+    CUDA_TRY(cudaMemcpyAsync(fields, p->d_fields, sizeof(double) * 2 * p->n, cudaMemcpyDeviceToHost, p->stream));
     return sync_and_check(p);
 }
 
-int hs_quality(hs_plan *p, const double *phase, double *e, double *u, double *intensities,
-               double *relative, double *fields)
+int hs_quality(hs_plan *p, const double *phase, double *e, double *u, double *intensities, double *relative,
+               double *fields)
 {
     if (!(p->sum_amp > 0.0)) return fail(HS_EZEROILLUM, "pupil carries no illumination");
-    int rc = forward_common(p, phase, 0, p->m, UPD_FINAL);
-    if (rc) return rc;
+    int rc;
+    if ((rc = check_range(p, 0, p->m)) || (rc = check_device(p)) || (rc = ensure_tables(p)) ||
+        (rc = reset_status(p)))
+        return rc;
+    const DevList *dense;
+    if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(p->d_phase, phase, sizeof(double) * p->m, cudaMemcpyHostToDevice, p->stream));
+    {
+        OnePattern one(p);
+        rc = launch_pass(p, PM_FWD, *dense, 0, dense->count, 0, p->d_phase, nullptr, 0, upd_args(p, ACT_FINAL));
+        if (rc) return rc;
+    }
     int32_t qs = 0;
     CUDA_TRY(cudaMemcpyAsync(e, p->d_e, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
     CUDA_TRY(cudaMemcpyAsync(u, p->d_u, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
     CUDA_TRY(cudaMemcpyAsync(&qs, p->d_qstatus, sizeof(int32_t), cudaMemcpyDeviceToHost, p->stream));
     if (intensities)
-        CUDA_TRY(cudaMemcpyAsync(intensities, p->d_inten, sizeof(double) * p->n, cudaMemcpyDeviceToHost,
-                                 p->stream));
+        CUDA_TRY(cudaMemcpyAsync(intensities, p->d_inten, sizeof(double) * p->n, cudaMemcpyDeviceToHost, p->stream));
     if (relative)
-        CUDA_TRY(cudaMemcpyAsync(relative, p->d_rel, sizeof(double) * p->n, cudaMemcpyDeviceToHost,
-                                 p->stream));
+        CUDA_TRY(cudaMemcpyAsync(relative, p->d_rel, sizeof(double) * p->n, cudaMemcpyDeviceToHost, p->stream));
     if (fields)
-        CUDA_TRY(cudaMemcpyAsync(fields, p->d_fields, sizeof(double) * 2 * p->n, cudaMemcpyDeviceToHost,
-                                 p->stream));
+        CUDA_TRY(cudaMemcpyAsync(fields, p->d_fields, sizeof(double) * 2 * p->n, cudaMemcpyDeviceToHost, p->stream));
     if ((rc = sync_and_check(p))) return rc;
     if (qs) return fail(HS_EUNDEFINED, "all spot intensities are zero");
     return HS_OK;
@@ -695,17 +747,17 @@ int hs_solve_async(hs_plan *p, int alg, int iters, int64_t subset, const double 
         if (alg == HS_ALG_WGS) subset = p->m;
         if (subset < 1 || subset > p->m) return fail(HS_EINVAL, "subset size %lld outside 1..M", (long long)subset);
     }
-    if ((flags & HS_WANT_FIELDS) && !(p->sum_amp > 0.0))
-        return fail(HS_EZEROILLUM, "pupil carries no illumination");
+    if ((flags & HS_WANT_FIELDS) && !(p->sum_amp > 0.0)) return fail(HS_EZEROILLUM, "pupil carries no illumination");
     int rc;
-    if ((rc = check_device(p))) return rc;
-    if ((rc = ensure_trace(p, iters))) return rc;
-    // windows are built (host sort + upload) outside capture
+    if ((rc = check_device(p)) || (rc = ensure_trace(p, iters))) return rc;
+    // host-side list building happens outside graph capture
+    const DevList *l;
+    if ((rc = get_dense(p, p->cfg.spw, &l))) return rc;
     if (alg != HS_ALG_RS && subset < p->m && iters > 2) {
         const int64_t half = std::max<int64_t>(1, subset / 2);
-        for (int j = 1; j <= iters - 2; ++j) {
-            const DevList *l;
-            if ((rc = get_window(p, ((int64_t)(j - 1) * half) % (p->m - subset + 1), subset, &l))) return rc;
+        for (int j = 0; j <= iters - 2; ++j) {
+            const int64_t off = j == 0 ? 0 : ((int64_t)(j - 1) * half) % (p->m - subset + 1);
+            if ((rc = get_window(p, off, subset, &l))) return rc;
         }
     }
     const size_t bytes = sizeof(double) * (size_t)p->batch * p->n;
@@ -714,7 +766,6 @@ int hs_solve_async(hs_plan *p, int alg, int iters, int64_t subset, const double 
     auto it = p->graphs.find(key);
     if (it == p->graphs.end()) {
         cudaGraph_t graph;
-        p->launches = 0;
         CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
         rc = record_solve(p, alg, iters, subset, flags);
         cudaError_t ce = cudaStreamEndCapture(p->stream, &graph);
@@ -725,20 +776,13 @@ int hs_solve_async(hs_plan *p, int alg, int iters, int64_t subset, const double 
         cudaGraphDestroy(graph);
         if (ce != cudaSuccess) return fail(HS_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
         it = p->graphs.emplace(key, exec).first;
-        p->last_launches = p->launches;
     }
     CUDA_TRY(cudaGraphLaunch(it->second, p->stream));
     p->tables_valid = true;
     p->last_alg = alg;
     p->last_iters = iters;
     p->last_flags = flags;
-    {
-        // launches recorded for this key: recount cheaply from the schedule
-        int64_t l = 3;  // tables + seed + first pass
-        if (alg != HS_ALG_RS) l += 2LL * iters;
-        if (flags & HS_WANT_FIELDS) l += 1;
-        p->last_launches = l;
-    }
+    p->last_launches = (alg == HS_ALG_RS) ? 2 : 2 + iters;  // tables(+seed) + passes
     return HS_OK;
 }
 
@@ -761,11 +805,10 @@ int hs_get_status(hs_plan *p, int32_t *status, int32_t *degenerate)
     int rc;
     if ((rc = check_device(p))) return rc;
     if (status)
-        CUDA_TRY(cudaMemcpyAsync(status, p->d_status, sizeof(int32_t) * p->batch, cudaMemcpyDeviceToHost,
-                                 p->stream));
+        CUDA_TRY(cudaMemcpyAsync(status, p->d_status, sizeof(int32_t) * p->batch, cudaMemcpyDeviceToHost, p->stream));
     if (degenerate)
-        CUDA_TRY(cudaMemcpyAsync(degenerate, p->d_degen, sizeof(int32_t) * p->batch,
-                                 cudaMemcpyDeviceToHost, p->stream));
+        CUDA_TRY(cudaMemcpyAsync(degenerate, p->d_degen, sizeof(int32_t) * p->batch, cudaMemcpyDeviceToHost,
+                                 p->stream));
     return sync_and_check(p);
 }
 
@@ -776,11 +819,9 @@ int hs_get_trace(hs_plan *p, double *weights, double *mags)
     const size_t cnt = (size_t)p->batch * p->last_iters * p->n;
     if (cnt) {
         if (weights)
-            CUDA_TRY(cudaMemcpyAsync(weights, p->d_trace_w, sizeof(double) * cnt, cudaMemcpyDeviceToHost,
-                                     p->stream));
+            CUDA_TRY(cudaMemcpyAsync(weights, p->d_trace_w, sizeof(double) * cnt, cudaMemcpyDeviceToHost, p->stream));
         if (mags)
-            CUDA_TRY(cudaMemcpyAsync(mags, p->d_trace_m, sizeof(double) * cnt, cudaMemcpyDeviceToHost,
-                                     p->stream));
+            CUDA_TRY(cudaMemcpyAsync(mags, p->d_trace_m, sizeof(double) * cnt, cudaMemcpyDeviceToHost, p->stream));
     }
     return sync_and_check(p);
 }
@@ -821,8 +862,8 @@ int hs_solve_host(hs_plan *p, int alg, int iters, int64_t subset, int batch, int
     if ((rc = hs_set_spots(p, batch, n, x, y, z, a0))) return rc;
     if ((rc = hs_solve_async(p, alg, iters, subset, theta0, HS_WANT_FIELDS))) return rc;
     if (phase)
-        CUDA_TRY(cudaMemcpyAsync(phase, p->d_phase, sizeof(double) * (size_t)batch * p->m,
-                                 cudaMemcpyDeviceToHost, p->stream));
+        CUDA_TRY(cudaMemcpyAsync(phase, p->d_phase, sizeof(double) * (size_t)batch * p->m, cudaMemcpyDeviceToHost,
+                                 p->stream));
     if (e) CUDA_TRY(cudaMemcpyAsync(e, p->d_e, sizeof(double) * batch, cudaMemcpyDeviceToHost, p->stream));
     if (u) CUDA_TRY(cudaMemcpyAsync(u, p->d_u, sizeof(double) * batch, cudaMemcpyDeviceToHost, p->stream));
     return sync_and_check(p);
@@ -836,6 +877,8 @@ int hs_last_launch_count(hs_plan *p, int64_t *launches)
     return HS_OK;
 }
 
+// which: 0 = full-range fused pass (dense list), 1 = compressed-window fused
+// pass over storage window [0, subset); both with the fold (ACT_FIELDS).
 int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_per_launch,
                    double *pairs_per_launch)
 {
@@ -843,36 +886,24 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
     if (reps < 1) return fail(HS_EINVAL, "reps must be >= 1");
     int rc;
     if ((rc = check_device(p)) || (rc = ensure_tables(p))) return rc;
-    const DevList *l = &p->dense;
-    if (which == 1) {
+    const DevList *l;
+    if (which == 0) {
+        rc = get_dense(p, p->cfg.spw, &l);
+    } else {
         if (subset < 1 || subset > p->m) return fail(HS_EINVAL, "subset invalid");
-        if ((rc = get_window(p, 0, subset, &l))) return rc;
+        rc = get_window(p, 0, subset, &l);
     }
-    if ((rc = ensure_trace(p, 1))) return rc;
+    if (rc) return rc;
     cudaEvent_t e0, e1;
     CUDA_TRY(cudaEventCreate(&e0));
     CUDA_TRY(cudaEventCreate(&e1));
-    int32_t nch = 0;
-    auto once = [&]() -> int {
-        if (which == 2) {
-            UpdArgs u = upd_args(p, UPD_STEP, nch);
-            u.iter = 0;
-            u.iters = 1;
-            return launch_update(p, u);
-        }
-        return launch_pass(p, PM_BWD | PM_FWD, l->rc, l->amp, nullptr, 0, l->count, nullptr, nullptr, 0, &nch);
-    };
-    if (which == 2) {
-        // make the update meaningful: produce partials once
-        if ((rc = launch_pass(p, PM_BWD | PM_FWD, l->rc, l->amp, nullptr, 0, l->count, nullptr, nullptr, 0,
-                              &nch)))
-            return rc;
-    }
-    if ((rc = reset_status(p)) || (rc = once()) || (rc = reset_status(p))) return rc;
+    const UpdArgs u = upd_args(p, ACT_FIELDS);
+    if ((rc = reset_status(p)) ||
+        (rc = launch_pass(p, PM_BWD | PM_FWD, *l, 0, l->count, 0, nullptr, nullptr, 0, u)))
+        return rc;
     CUDA_TRY(cudaEventRecord(e0, p->stream));
-    for (int r = 0; r < reps; ++r) {
-        if ((rc = once())) return rc;
-    }
+    for (int r = 0; r < reps; ++r)
+        if ((rc = launch_pass(p, PM_BWD | PM_FWD, *l, 0, l->count, 0, nullptr, nullptr, 0, u))) return rc;
     CUDA_TRY(cudaEventRecord(e1, p->stream));
     CUDA_TRY(cudaEventSynchronize(e1));
     float ms = 0.f;
@@ -880,8 +911,9 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *ms_per_launch = ms / reps;
-    *pairs_per_launch = (which == 2) ? 0.0 : (double)l->count * p->n * p->batch;
-    return reset_status(p);
+    const int64_t pixels = (which == 0) ? p->m : subset;
+    *pairs_per_launch = (double)pixels * p->n * p->batch;
+    return HS_OK;
 }
 
 void *hs_host_alloc(int64_t bytes)

@@ -174,6 +174,9 @@ summary["compression_runs"] = rows
 summary["grid36"] = spots_dict_list = {k: v.tolist() for k, v in
                                        spots_dict(grid36).items()}
 summary["grid100"] = {k: v.tolist() for k, v in spots_dict(grid100).items()}
+# compare_at_budget runs seed k on rotation frame k (bench.py:183-200)
+summary["grid36_frames"] = [{k: v.tolist() for k, v in spots_dict(f).items()}
+                            for f in hs.rotation_sweep(hs.named_scenario("grid36"), 5)]
 
 with open(os.path.join(HERE, "golden.json"), "w") as fh:
     json.dump(summary, fh, indent=1, default=float)

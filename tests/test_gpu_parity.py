@@ -186,9 +186,11 @@ def test_quality_gate_grid100(golden, pupils):
 def test_compression_golden_table(golden, pupils):
     """Reference demo table (demos/output/compression_runs.csv rows 2-41)."""
     p = pupils["p256u0"]
-    s = hs.named_spots("grid36")
+    frames = [hs.SpotSet(x=f["x"], y=f["y"], z=f["z"], amplitude=f["a0"])
+              for f in golden["grid36_frames"]]
     worst = {}
     for row in golden["compression_runs"]:
+        s = frames[row["seed"]]
         cfg = hs.SolverConfig(row["algorithm"], iterations=row["iterations"],
                               compression=row["c"], seed=row["seed"])
         holo, trace = hs.solve(p, s, cfg)
@@ -254,7 +256,7 @@ def test_large_spot_count_path(pupils, rng):
     s = hs.SpotSet(x=rng.uniform(-1e-4, 1e-4, 600), y=rng.uniform(-1e-4, 1e-4, 600),
                    z=rng.uniform(-5e-5, 5e-5, 600), amplitude=np.ones(600))
     holo, trace = hs.wgs(p, s, iterations=3, seed=1)
-    r = oracle.solve(p, s.x, s.y, s.z, s.amplitude, "wgs", 3)
+    r = oracle.solve(p, s.x, s.y, s.z, s.amplitude, "wgs", 3, seed=1)
     mags = np.array([rec.magnitudes for rec in trace.records])
     assert np.all(np.abs(mags - r["mags"]) <= 1e-4 * r["mags"])
     masked_phase_check(p, s, holo.phase, r["amps"], r["thetas"], tab=r["tables"])
