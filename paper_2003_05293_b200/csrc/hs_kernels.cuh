@@ -117,7 +117,7 @@ __device__ __forceinline__ void hs_seed_one(int b, int k, int n, int np, const d
 // y_n; the argument is formed with explicit round-to-nearest fp64 ops in the
 // reference order ((c1*x)*v + (c2*z)*v2) -> numba's bits; fp64 sincos; one
 // rounding to fp32.  Block (0, b) also seeds pattern b when seed_theta != 0.
-__global__ void hs_tables_kernel(int side, int np, int n, const double *__restrict__ axis,
+static __global__ void hs_tables_kernel(int side, int np, int n, const double *__restrict__ axis,
                                  double c1, double c2, const double *__restrict__ x,
                                  const double *__restrict__ y, const double *__restrict__ z,
                                  float2 *__restrict__ gx, float2 *__restrict__ gy,
@@ -149,7 +149,7 @@ __global__ void hs_tables_kernel(int side, int np, int n, const double *__restri
     }
 }
 
-__global__ void hs_seed_kernel(int n, int np, const double *amp, const double *theta, float2 *coef,
+static __global__ void hs_seed_kernel(int n, int np, const double *amp, const double *theta, float2 *coef,
                                double *w)
 {
     for (int k = threadIdx.x; k < np; k += blockDim.x) hs_seed_one(blockIdx.x, k, n, np, amp, theta, coef, w);
@@ -354,8 +354,7 @@ hs_pass_kernel(const PassArgs a)
     const int lane = tid & 31, warp = tid >> 5;
     const int g = lane % G, s = lane / G;
     const int slot = warp * SPW + s;
-    const int npv = a.np >> 1;     // float4 per table row
-    const int nv = a.nl >> 1;      // active float4 per lane
+    constexpr int npv = G * NV;    // float4 per table row (np = G * NL)
     float4 *coef_s = smem4;                  // [npv]
     float4 *E_s = smem4 + npv;               // [NSLOT][npv]
 
@@ -370,25 +369,28 @@ hs_pass_kernel(const PassArgs a)
     const float4 *__restrict__ X = reinterpret_cast<const float4 *>(a.gx + (int64_t)pat * a.tab_stride) + g;
     const float4 *__restrict__ Y = reinterpret_cast<const float4 *>(a.gy + (int64_t)pat * a.tab_stride) + g;
 
+    // V = coef * gy[row] (backward), T = sum_p b_p gx[c_p] (forward), per row.
     float vr[NL], vi[NL], tr[NL], ti[NL];
 #pragma unroll
     for (int k = 0; k < NL; ++k) { vr[k] = 0.f; vi[k] = 0.f; tr[k] = 0.f; ti[k] = 0.f; }
 
     auto flush = [&](int r) {
-        // E_slot += gy[r] * T, T = 0
+        // E_slot += gy[r] * T ; T = 0
         const float4 *yr = Y + (int64_t)r * npv;
         float4 *es = E_s + slot * npv + g;
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-            if (j < nv) {
-                const float4 q = __ldg(yr + G * j);
-                float4 e = es[G * j];
-                e.x += q.x * tr[2 * j] - q.y * ti[2 * j];
-                e.y += q.x * ti[2 * j] + q.y * tr[2 * j];
-                e.z += q.z * tr[2 * j + 1] - q.w * ti[2 * j + 1];
-                e.w += q.z * ti[2 * j + 1] + q.w * tr[2 * j + 1];
-                es[G * j] = e;
-            }
+            const float4 q = __ldg(yr + G * j);
+            float4 e = es[G * j];
+            e.x = fmaf(q.x, tr[2 * j], e.x);
+            e.x = fmaf(-q.y, ti[2 * j], e.x);
+            e.y = fmaf(q.x, ti[2 * j], e.y);
+            e.y = fmaf(q.y, tr[2 * j], e.y);
+            e.z = fmaf(q.z, tr[2 * j + 1], e.z);
+            e.z = fmaf(-q.w, ti[2 * j + 1], e.z);
+            e.w = fmaf(q.z, ti[2 * j + 1], e.w);
+            e.w = fmaf(q.w, tr[2 * j + 1], e.w);
+            es[G * j] = e;
             tr[2 * j] = 0.f; ti[2 * j] = 0.f; tr[2 * j + 1] = 0.f; ti[2 * j + 1] = 0.f;
         }
     };
@@ -416,12 +418,12 @@ hs_pass_kernel(const PassArgs a)
                 const float4 *cs = coef_s + g;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
-                    float4 q = make_float4(0.f, 0.f, 0.f, 0.f), k4 = q;
-                    if (j < nv) { q = __ldg(yr + G * j); k4 = cs[G * j]; }
-                    vr[2 * j] = k4.x * q.x - k4.y * q.y;
-                    vi[2 * j] = k4.x * q.y + k4.y * q.x;
-                    vr[2 * j + 1] = k4.z * q.z - k4.w * q.w;
-                    vi[2 * j + 1] = k4.z * q.w + k4.w * q.z;
+                    const float4 q = __ldg(yr + G * j);
+                    const float4 k4 = cs[G * j];
+                    vr[2 * j] = fmaf(k4.x, q.x, -k4.y * q.y);
+                    vi[2 * j] = fmaf(k4.x, q.y, k4.y * q.x);
+                    vr[2 * j + 1] = fmaf(k4.z, q.z, -k4.w * q.w);
+                    vi[2 * j + 1] = fmaf(k4.z, q.w, k4.w * q.z);
                 }
             }
             rcur = r;
@@ -430,8 +432,7 @@ hs_pass_kernel(const PassArgs a)
         const float4 *xc = X + (int64_t)c * npv;
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-            float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (j < nv) q = __ldg(xc + G * j);
+            const float4 q = __ldg(xc + G * j);
             xr[2 * j] = q.x; xi[2 * j] = q.y; xr[2 * j + 1] = q.z; xi[2 * j + 1] = q.w;
         }
 
@@ -440,10 +441,14 @@ hs_pass_kernel(const PassArgs a)
             float s0r = 0.f, s0i = 0.f, s1r = 0.f, s1i = 0.f;
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
-                s0r += vr[2 * j] * xr[2 * j] - vi[2 * j] * xi[2 * j];
-                s0i += vr[2 * j] * xi[2 * j] + vi[2 * j] * xr[2 * j];
-                s1r += vr[2 * j + 1] * xr[2 * j + 1] - vi[2 * j + 1] * xi[2 * j + 1];
-                s1i += vr[2 * j + 1] * xi[2 * j + 1] + vi[2 * j + 1] * xr[2 * j + 1];
+                s0r = fmaf(vr[2 * j], xr[2 * j], s0r);
+                s0r = fmaf(-vi[2 * j], xi[2 * j], s0r);
+                s0i = fmaf(vr[2 * j], xi[2 * j], s0i);
+                s0i = fmaf(vi[2 * j], xr[2 * j], s0i);
+                s1r = fmaf(vr[2 * j + 1], xr[2 * j + 1], s1r);
+                s1r = fmaf(-vi[2 * j + 1], xi[2 * j + 1], s1r);
+                s1i = fmaf(vr[2 * j + 1], xi[2 * j + 1], s1i);
+                s1i = fmaf(vi[2 * j + 1], xr[2 * j + 1], s1i);
             }
             float sr = s0r + s1r, si = s0i + s1i;
             // Butterfly over the G lanes of the pixel (a+b == b+a: all lanes
@@ -454,17 +459,17 @@ hs_pass_kernel(const PassArgs a)
                 si += __shfl_xor_sync(0xffffffffu, si, o);
             }
             // b = A e^{-i arg S} = A conj(S)/|S|; arg(0) = 0 (kernels.py:115-119)
-            const float m2 = sr * sr + si * si;
+            const float m2 = fmaf(sr, sr, si * si);
             if (m2 > 0.f && m2 < INFINITY) {
-                const float inv = rsqrtf(m2);
-                br = A * (sr * inv);
-                bi = -A * (si * inv);
+                const float inv = A * rsqrtf(m2);
+                br = sr * inv;
+                bi = -si * inv;
             } else if (sr != 0.f || si != 0.f) {
                 const float mx = fmaxf(fabsf(sr), fabsf(si));
                 const float xr_ = sr / mx, xi_ = si / mx;
-                const float inv = rsqrtf(xr_ * xr_ + xi_ * xi_);
-                br = A * (xr_ * inv);
-                bi = -A * (xi_ * inv);
+                const float inv = A * rsqrtf(fmaf(xr_, xr_, xi_ * xi_));
+                br = xr_ * inv;
+                bi = -xi_ * inv;
             } else {
                 br = A;
                 bi = 0.f;
@@ -494,8 +499,10 @@ hs_pass_kernel(const PassArgs a)
         if (FWD) {
 #pragma unroll
             for (int k = 0; k < NL; ++k) {
-                tr[k] += br * xr[k] - bi * xi[k];
-                ti[k] += br * xi[k] + bi * xr[k];
+                tr[k] = fmaf(br, xr[k], tr[k]);
+                tr[k] = fmaf(-bi, xi[k], tr[k]);
+                ti[k] = fmaf(br, xi[k], ti[k]);
+                ti[k] = fmaf(bi, xr[k], ti[k]);
             }
         }
     }
@@ -508,6 +515,7 @@ hs_pass_kernel(const PassArgs a)
         float2 *out = a.partials + (int64_t)pat * a.part_stride + (int64_t)chunk * a.np;
         for (int k = tid; k < a.np; k += kThreads) {
             float sx = 0.f, sy = 0.f;
+#pragma unroll 8
             for (int q = 0; q < NSLOT; ++q) {
                 const float2 v = E2[q * a.np + k];
                 sx += v.x;
@@ -521,5 +529,41 @@ hs_pass_kernel(const PassArgs a)
         }
     }
 }
+
+// Kernel selection (instantiated per G in hs_pass_g*.cu).
+typedef void (*PassFn)(PassArgs);
+
+template <int G, int NL>
+PassFn hs_pass_fn(int mode)
+{
+    switch (mode) {
+    case PM_BWD | PM_WRITE: return hs_pass_kernel<G, NL, PM_BWD | PM_WRITE>;
+    case PM_FWD: return hs_pass_kernel<G, NL, PM_FWD>;
+    case PM_BWD | PM_FWD: return hs_pass_kernel<G, NL, PM_BWD | PM_FWD>;
+    case PM_BWD | PM_FWD | PM_WRITE: return hs_pass_kernel<G, NL, PM_BWD | PM_FWD | PM_WRITE>;
+    default: return nullptr;
+    }
+}
+
+PassFn hs_select_g1(int nl, int mode);
+PassFn hs_select_g2(int nl, int mode);
+PassFn hs_select_g4(int nl, int mode);
+PassFn hs_select_g8(int nl, int mode);
+PassFn hs_select_g16(int nl, int mode);
+PassFn hs_select_g32(int nl, int mode);
+
+#define HS_DEFINE_SELECT(GV)                                  \
+    PassFn hs_select_g##GV(int nl, int mode)                  \
+    {                                                         \
+        switch (nl) {                                         \
+        case 4: return hs_pass_fn<GV, 4>(mode);               \
+        case 8: return hs_pass_fn<GV, 8>(mode);               \
+        case 10: return hs_pass_fn<GV, 10>(mode);             \
+        case 12: return hs_pass_fn<GV, 12>(mode);             \
+        case 14: return hs_pass_fn<GV, 14>(mode);             \
+        case 16: return hs_pass_fn<GV, 16>(mode);             \
+        default: return nullptr;                              \
+        }                                                     \
+    }
 
 }  // namespace hs

@@ -1,0 +1,6 @@
+// Instantiates hs_pass_kernel for G = 2 lanes per pixel (see hs_kernels.cuh).
+#include "hs_kernels.cuh"
+
+namespace hs {
+HS_DEFINE_SELECT(2)
+}  // namespace hs

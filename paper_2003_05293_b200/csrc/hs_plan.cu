@@ -74,9 +74,9 @@ void dfree(T *&p)
     p = nullptr;
 }
 
-// G lanes per pixel, NLMAX spots per lane (template), nl active (even).
+// G lanes per pixel, NL spots per lane (a template value), np = G * NL.
 struct Config {
-    int G, NLMAX, nl, np, spw;
+    int G, NL, np, spw;
 };
 
 Config pick_config(int n)
@@ -84,38 +84,28 @@ Config pick_config(int n)
     Config c{};
     c.G = 1;
     while (c.G < 32 && (n + c.G - 1) / c.G > 16) c.G *= 2;
-    c.NLMAX = ((n + c.G - 1) / c.G > 16) ? 32 : 16;
-    c.nl = (n + c.G - 1) / c.G;
-    c.nl += c.nl & 1;
-    c.np = c.G * c.nl;
+    int nl = (n + c.G - 1) / c.G;
+    nl += nl & 1;
+    const int choices[] = {4, 8, 10, 12, 14, 16, 32};
+    for (int v : choices)
+        if (v >= nl) {
+            c.NL = v;
+            break;
+        }
+    c.np = c.G * c.NL;
     c.spw = 32 / c.G;
     return c;
 }
 
-typedef void (*PassFn)(PassArgs);
-
-template <int G, int NL>
-PassFn pass_fn(int mode)
-{
-    switch (mode) {
-    case PM_BWD | PM_WRITE: return hs_pass_kernel<G, NL, PM_BWD | PM_WRITE>;
-    case PM_FWD: return hs_pass_kernel<G, NL, PM_FWD>;
-    case PM_BWD | PM_FWD: return hs_pass_kernel<G, NL, PM_BWD | PM_FWD>;
-    case PM_BWD | PM_FWD | PM_WRITE: return hs_pass_kernel<G, NL, PM_BWD | PM_FWD | PM_WRITE>;
-    default: return nullptr;
-    }
-}
-
 PassFn select_pass(const Config &c, int mode)
 {
-    if (c.NLMAX == 32) return pass_fn<32, 32>(mode);
     switch (c.G) {
-    case 1: return pass_fn<1, 16>(mode);
-    case 2: return pass_fn<2, 16>(mode);
-    case 4: return pass_fn<4, 16>(mode);
-    case 8: return pass_fn<8, 16>(mode);
-    case 16: return pass_fn<16, 16>(mode);
-    default: return pass_fn<32, 16>(mode);
+    case 1: return hs_select_g1(c.NL, mode);
+    case 2: return hs_select_g2(c.NL, mode);
+    case 4: return hs_select_g4(c.NL, mode);
+    case 8: return hs_select_g8(c.NL, mode);
+    case 16: return hs_select_g16(c.NL, mode);
+    default: return hs_select_g32(c.NL, mode);
     }
 }
 
@@ -441,7 +431,7 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
     a.chunk_len = geo.chunk_len;
     a.nchunks = geo.nchunks;
     a.np = c.np;
-    a.nl = c.nl;
+    a.nl = c.NL;
     a.tab_stride = (int64_t)p->side * c.np;
     a.gx = p->d_gx;
     a.gy = p->d_gy;
@@ -594,9 +584,9 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
     if ((rc = build_storage(p.get()))) return rc;
     const int modes[4] = {PM_BWD | PM_WRITE, PM_FWD, PM_BWD | PM_FWD, PM_BWD | PM_FWD | PM_WRITE};
     for (int mode : modes) {
-        Config c{32, 32, 32, 1024, 1};
-        CUDA_TRY(cudaFuncSetAttribute(select_pass(c, mode), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)pass_smem(c)));
+        Config c{32, 32, 1024, 1};
+        CUDA_TRY(cudaFuncSetAttribute((const void *)select_pass(c, mode),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(c)));
     }
     *out = p.release();
     return HS_OK;
