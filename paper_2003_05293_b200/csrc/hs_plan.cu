@@ -54,6 +54,7 @@ struct DevList {
     int32_t *dst = nullptr;
     int64_t count = 0;
     int32_t chunk_len = 0;  // 0: choose from kTargetChunks
+    int32_t sorted_rows = 0;
 };
 
 template <typename T>
@@ -109,10 +110,7 @@ PassFn select_pass(const Config &c, int mode)
     }
 }
 
-size_t pass_smem(const Config &c)
-{
-    return (size_t)c.np * sizeof(float2) * (1 + kThreads / c.G);
-}
+size_t pass_smem(const Config &c) { return hs_pass_smem_bytes(c.G, c.NL); }
 
 }  // namespace
 
@@ -263,6 +261,7 @@ int get_window(hs_plan *p, int64_t start, int64_t count, const DevList **out)
         DevList l;
         int r = upload_entries(rc, amp, nullptr, 0, &l);
         if (r) return r;
+        l.sorted_rows = 1;
         it = p->windows.emplace(key, l).first;
     }
     *out = &it->second;
@@ -282,7 +281,7 @@ Geom geom_of(const DevList &l, int64_t count, int spw)
         const int64_t unit = (int64_t)kWarps * spw;
         int64_t per = (count + kTargetChunks - 1) / kTargetChunks;
         per = ((per + unit - 1) / unit) * unit;
-        g.chunk_len = (int32_t)std::max<int64_t>(per, unit);
+        g.chunk_len = (int32_t)std::min<int64_t>(std::max<int64_t>(per, unit), kMaxChunk);
     }
     g.nchunks = (int32_t)((count + g.chunk_len - 1) / g.chunk_len);
     return g;
@@ -432,6 +431,7 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
     a.nchunks = geo.nchunks;
     a.np = c.np;
     a.nl = c.NL;
+    a.sorted_rows = l.sorted_rows;
     a.tab_stride = (int64_t)p->side * c.np;
     a.gx = p->d_gx;
     a.gy = p->d_gy;
@@ -583,11 +583,16 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
     CUDA_TRY(cudaMemcpy(p->d_axis, axis, sizeof(double) * side, cudaMemcpyHostToDevice));
     if ((rc = build_storage(p.get()))) return rc;
     const int modes[4] = {PM_BWD | PM_WRITE, PM_FWD, PM_BWD | PM_FWD, PM_BWD | PM_FWD | PM_WRITE};
-    for (int mode : modes) {
-        Config c{32, 32, 1024, 1};
-        CUDA_TRY(cudaFuncSetAttribute((const void *)select_pass(c, mode),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(c)));
-    }
+    const int gs[6] = {1, 2, 4, 8, 16, 32};
+    const int nls[7] = {4, 8, 10, 12, 14, 16, 32};
+    for (int G : gs)
+        for (int NL : nls) {
+            if (NL == 32 && G != 32) continue;
+            Config c{G, NL, G * NL, 32 / G};
+            for (int mode : modes)
+                CUDA_TRY(cudaFuncSetAttribute((const void *)select_pass(c, mode),
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(c)));
+        }
     *out = p.release();
     return HS_OK;
 }
@@ -620,7 +625,8 @@ int hs_set_spots(hs_plan *p, int batch, int n, const double *x, const double *y,
     p->cfg = pick_config(n);
     const DevList *dense;
     if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
-    const int64_t chunks = std::max<int64_t>(geom_of(*dense, dense->count, p->cfg.spw).nchunks, kTargetChunks + 1);
+    const int64_t chunks = std::max<int64_t>({(int64_t)geom_of(*dense, dense->count, p->cfg.spw).nchunks,
+                                              (int64_t)kTargetChunks + 1, p->m / kMaxChunk + 2});
     if ((rc = ensure_fold(p, chunks))) return rc;
     const size_t bytes = sizeof(double) * (size_t)batch * n;
     CUDA_TRY(cudaMemcpyAsync(p->d_x, x, bytes, cudaMemcpyHostToDevice, p->stream));
