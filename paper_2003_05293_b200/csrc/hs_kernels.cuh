@@ -61,22 +61,10 @@ struct UpdArgs {
     double *e, *u, *inten, *rel;  // [B], [B], [B][n], [B][n]
 };
 
-struct PassArgs {
-    const int32_t *rc;        // packed (row << 16) | col per list entry
-    const float *amp;         // illumination amplitude per entry (0: padding)
-    const int32_t *dst;       // storage index per entry, -1 padding (nullptr: i + idx_base)
-    int64_t idx_base;
-    int64_t count;            // list length
-    int32_t chunk_len;        // entries per CTA; multiple of 8 * SPW
-    int32_t nchunks;
-    int32_t np, nl;           // padded spot count, spots per lane (even)
-    int32_t sorted_rows;      // list is sorted by row (window lists): stage gy rows
-    int64_t tab_stride;       // side * np
-    const float2 *gx, *gy;    // [B][side][np]
-    const float2 *coef;       // [B][np]
-    const double *phase_in;   // [B][phase_stride] (PM_FWD without PM_BWD)
-    double *phase_out;        // [B][phase_stride] (PM_WRITE)
-    int64_t phase_stride;
+// Cross-CTA fold state shared by the pass and tile kernels.
+struct FoldArgs {
+    int32_t nchunks;          // partials per pattern in this launch
+    int32_t np;
     float2 *partials;         // [B][part_stride]: [chunk][np]
     int64_t part_stride;
     double2 *gpart;           // [B][gpart_stride]: [group][np]
@@ -85,6 +73,24 @@ struct PassArgs {
     int32_t *pat_cnt;         // [B]
     int32_t cnt_stride;
     UpdArgs u;
+};
+
+struct PassArgs {
+    const int32_t *rc;        // packed (row << 16) | col per list entry
+    const float *amp;         // illumination amplitude per entry (0: padding)
+    const int32_t *dst;       // storage index per entry, -1 padding (nullptr: i + idx_base)
+    int64_t idx_base;
+    int64_t count;            // list length
+    int32_t chunk_len;        // entries per CTA; multiple of 8 * SPW
+    int32_t np, nl;           // padded spot count, spots per lane (even)
+    int32_t sorted_rows;      // list is sorted by row (window lists): stage gy rows
+    int64_t tab_stride;       // side * np
+    const float2 *gx, *gy;    // [B][side][np]
+    const float2 *coef;       // [B][np]
+    const double *phase_in;   // [B][phase_stride] (PM_FWD without PM_BWD)
+    double *phase_out;        // [B][phase_stride] (PM_WRITE)
+    int64_t phase_stride;
+    FoldArgs f;
 };
 
 // ---------------------------------------------------------------------------
@@ -277,7 +283,7 @@ __device__ __forceinline__ void hs_update(const UpdArgs &a, int b, double2 *E, d
 // of each kGroup-chunk group folds the group in chunk order (fp64); the last
 // group-folder of the pattern folds the groups in order and applies the
 // action.  Counters reset themselves, so graphs replay without memsets.
-__device__ __forceinline__ void hs_fold(const PassArgs &a, int pat, int chunk, char *scratch)
+__device__ __forceinline__ void hs_fold(const FoldArgs &a, int pat, int chunk, char *scratch)
 {
     __shared__ int s_last;
     __shared__ double dbuf[kThreads];
@@ -335,30 +341,12 @@ __device__ __forceinline__ void hs_fold(const PassArgs &a, int pat, int chunk, c
 }
 
 // ---------------------------------------------------------------------------
-// cp.async (LDGSTS) helpers: 16-byte global -> shared copies tracked per thread.
-__device__ __forceinline__ void hs_cp16(void *smem, const void *gmem)
-{
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void hs_cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void hs_cp_wait()
-{
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
-// gx-row prefetch depth in trips (the 1024-spot variant has no room for two)
-__host__ __device__ constexpr int hs_stages(int NL) { return NL > 16 ? 1 : 2; }
-constexpr int kStageRows = 4;   // gy rows staged for row-sorted chunks
-constexpr int kMaxChunk = 2048; // largest chunk_len (list entries staged in smem)
+constexpr int kMaxChunk = 2048;  // largest chunk_len of auto-chunked lists
 
 // Dynamic shared memory of hs_pass_kernel for a (G, NL) configuration.
 __host__ __device__ constexpr size_t hs_pass_smem_bytes(int G, int NL)
 {
-    return sizeof(float2) * (size_t)G * NL *
-               (1 + (kThreads / G) * (1 + hs_stages(NL)) + kStageRows) +
-           (size_t)kMaxChunk * (sizeof(int32_t) + sizeof(float));
+    return sizeof(float2) * (size_t)G * NL * (1 + kThreads / G);
 }
 
 template <int G, int NL, int MODE>
@@ -368,8 +356,6 @@ hs_pass_kernel(const PassArgs a)
     constexpr int SPW = 32 / G;
     constexpr int NSLOT = kThreads / G;
     constexpr int NV = NL / 2;
-    constexpr int npv = G * NV;    // float4 per table row (np = G * NL)
-    constexpr int kStages = hs_stages(NL);
     constexpr bool BWD = (MODE & PM_BWD) != 0;
     constexpr bool FWD = (MODE & PM_FWD) != 0;
     constexpr bool WRITE = (MODE & PM_WRITE) != 0;
@@ -377,88 +363,39 @@ hs_pass_kernel(const PassArgs a)
 
     const int pat = blockIdx.y;
     const int chunk = blockIdx.x;
-    if (a.u.status[pat] != 0) return;  // pattern already failed (uniform per CTA)
+    if (a.f.u.status[pat] != 0) return;  // pattern already failed (uniform per CTA)
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int g = lane % G, s = lane / G;
     const int slot = warp * SPW + s;
-    // shared memory carve-up
-    float4 *coef_s = smem4;                          // [npv]
-    float4 *E_s = coef_s + npv;                      // [NSLOT][npv]
-    float4 *ring = E_s + NSLOT * npv;                // [NSLOT][kStages][npv]
-    float4 *gys = ring + NSLOT * kStages * npv;      // [kStageRows][npv]
-    int32_t *ent_rc = reinterpret_cast<int32_t *>(gys + kStageRows * npv);  // [kMaxChunk]
-    float *ent_amp = reinterpret_cast<float *>(ent_rc + kMaxChunk);         // [kMaxChunk]
+    constexpr int npv = G * NV;    // float4 per table row (np = G * NL)
+    float4 *coef_s = smem4;                  // [npv]
+    float4 *E_s = smem4 + npv;               // [NSLOT][npv]
 
-    const int64_t begin = (int64_t)chunk * a.chunk_len;
-    int64_t cend = begin + a.chunk_len;
-    if (cend > a.count) cend = a.count;
-    const int ccount = (int)(cend - begin);
-
-    const float4 *__restrict__ X = reinterpret_cast<const float4 *>(a.gx + (int64_t)pat * a.tab_stride) + g;
-    const float4 *__restrict__ Y = reinterpret_cast<const float4 *>(a.gy + (int64_t)pat * a.tab_stride);
-
-    // ---- prologue: coefficients, zeroed slot accumulators, list entries,
-    //      and (row-sorted chunks) the gy rows the chunk touches.
     if (BWD) {
         const float4 *cg = reinterpret_cast<const float4 *>(a.coef + (int64_t)pat * a.np);
         for (int k = tid; k < npv; k += kThreads) coef_s[k] = cg[k];
     }
     if (FWD)
         for (int k = tid; k < NSLOT * npv; k += kThreads) E_s[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k = tid; k < ccount; k += kThreads) {
-        ent_rc[k] = __ldg(a.rc + begin + k);
-        ent_amp[k] = __ldg(a.amp + begin + k);
-    }
-    int rfirst = 0, nstaged = 0;
-    if (a.sorted_rows && ccount > 0) {
-        rfirst = __ldg(a.rc + begin) >> 16;
-        const int rlast = __ldg(a.rc + cend - 1) >> 16;
-        if (rlast - rfirst + 1 <= kStageRows) {
-            nstaged = rlast - rfirst + 1;
-            for (int k = tid; k < nstaged * npv; k += kThreads)
-                gys[k] = __ldg(Y + (int64_t)(rfirst + k / npv) * npv + k % npv);
-        }
-    }
     __syncthreads();
 
-    const int wseg = a.chunk_len / kWarps;
-    const int wb = warp * wseg;                       // warp segment in chunk-local indices
-    const int we = min(wb + wseg, ccount);
-    const int trips = (we > wb) ? (we - wb + SPW - 1) / SPW : 0;
-    float4 *myring = ring + slot * (kStages * npv) + g;
-
-    auto prefetch = [&](int t) {
-        if (t < trips) {
-            const int li = wb + t * SPW + s;
-            const int c = (li < we) ? (ent_rc[li] & 0xffff) : 0;
-            const float4 *src = X + (int64_t)c * npv;
-            float4 *dst = myring + (t % kStages) * npv;
-#pragma unroll
-            for (int j = 0; j < NV; ++j) hs_cp16(dst + G * j, src + G * j);
-        }
-        hs_cp_commit();
-    };
-#pragma unroll
-    for (int t = 0; t < kStages - 1; ++t) prefetch(t);
+    const float4 *__restrict__ X = reinterpret_cast<const float4 *>(a.gx + (int64_t)pat * a.tab_stride) + g;
+    const float4 *__restrict__ Y = reinterpret_cast<const float4 *>(a.gy + (int64_t)pat * a.tab_stride) + g;
 
     // V = coef * gy[row] (backward), T = sum_p b_p gx[c_p] (forward), per row.
     float vr[NL], vi[NL], tr[NL], ti[NL];
 #pragma unroll
     for (int k = 0; k < NL; ++k) { vr[k] = 0.f; vi[k] = 0.f; tr[k] = 0.f; ti[k] = 0.f; }
 
-    auto gy_row = [&](int r) -> const float4 * {
-        const int off = r - rfirst;
-        return (off >= 0 && off < nstaged) ? gys + off * npv + g : Y + (int64_t)r * npv + g;
-    };
     auto flush = [&](int r) {
         // E_slot += gy[r] * T ; T = 0
-        const float4 *yr = gy_row(r);
+        const float4 *yr = Y + (int64_t)r * npv;
         float4 *es = E_s + slot * npv + g;
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-            const float4 q = yr[G * j];
+            const float4 q = __ldg(yr + G * j);
             float4 e = es[G * j];
             e.x = fmaf(q.x, tr[2 * j], e.x);
             e.x = fmaf(-q.y, ti[2 * j], e.x);
@@ -473,23 +410,30 @@ hs_pass_kernel(const PassArgs a)
         }
     };
 
+    const int64_t begin = (int64_t)chunk * a.chunk_len;
+    const int wseg = a.chunk_len / kWarps;
+    const int64_t wbegin = begin + (int64_t)warp * wseg;
+    int64_t wend = wbegin + wseg;
+    if (wend > a.count) wend = a.count;
+    const int trips = (wend > wbegin) ? (int)((wend - wbegin + SPW - 1) / SPW) : 0;
     int rcur = -1;
+
     for (int t = 0; t < trips; ++t) {
-        prefetch(t + kStages - 1);
-        const int li = wb + t * SPW + s;
-        const bool valid = li < we;
+        const int64_t i = wbegin + (int64_t)t * SPW + s;
+        const bool valid = i < wend;
         int rc = 0;
         float A = 0.f;
-        if (valid) { rc = ent_rc[li]; A = ent_amp[li]; }
+        if (valid) { rc = __ldg(a.rc + i); A = __ldg(a.amp + i); }
         const int r = valid ? (rc >> 16) : rcur;
+        const int c = valid ? (rc & 0xffff) : 0;
         if (r != rcur && r >= 0) {
             if (FWD && rcur >= 0) flush(rcur);
             if (BWD) {
-                const float4 *yr = gy_row(r);
+                const float4 *yr = Y + (int64_t)r * npv;
                 const float4 *cs = coef_s + g;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
-                    const float4 q = yr[G * j];
+                    const float4 q = __ldg(yr + G * j);
                     const float4 k4 = cs[G * j];
                     vr[2 * j] = fmaf(k4.x, q.x, -k4.y * q.y);
                     vi[2 * j] = fmaf(k4.x, q.y, k4.y * q.x);
@@ -499,12 +443,11 @@ hs_pass_kernel(const PassArgs a)
             }
             rcur = r;
         }
-        hs_cp_wait<kStages - 1>();
         float xr[NL], xi[NL];
-        const float4 *xc = myring + (t % kStages) * npv;
+        const float4 *xc = X + (int64_t)c * npv;
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-            const float4 q = xc[G * j];
+            const float4 q = __ldg(xc + G * j);
             xr[2 * j] = q.x; xi[2 * j] = q.y; xr[2 * j + 1] = q.z; xi[2 * j + 1] = q.w;
         }
 
@@ -547,8 +490,7 @@ hs_pass_kernel(const PassArgs a)
                 bi = 0.f;
             }
             if (WRITE && valid && g == 0) {
-                const int64_t gi = begin + li;
-                const int64_t di = a.dst ? (int64_t)a.dst[gi] : gi + a.idx_base;
+                const int64_t di = a.dst ? (int64_t)a.dst[i] : i + a.idx_base;
                 if (di >= 0) {
                     double ph = 0.0;
                     if (sr != 0.f || si != 0.f) {
@@ -562,8 +504,7 @@ hs_pass_kernel(const PassArgs a)
         } else {
             double sn = 0.0, cs = 1.0;
             if (valid) {
-                const int64_t gi = begin + li;
-                const int64_t di = a.dst ? (int64_t)a.dst[gi] : gi + a.idx_base;
+                const int64_t di = a.dst ? (int64_t)a.dst[i] : i + a.idx_base;
                 if (di >= 0) sincos(a.phase_in[(int64_t)pat * a.phase_stride + di], &sn, &cs);
             }
             br = A * (float)cs;
@@ -580,14 +521,13 @@ hs_pass_kernel(const PassArgs a)
             }
         }
     }
-    hs_cp_wait<0>();
 
     if (FWD) {
         if (rcur >= 0) flush(rcur);
         __syncthreads();
         // per-chunk partial: slots folded in slot order (fixed)
         const float2 *E2 = reinterpret_cast<const float2 *>(E_s);
-        float2 *out = a.partials + (int64_t)pat * a.part_stride + (int64_t)chunk * a.np;
+        float2 *out = a.f.partials + (int64_t)pat * a.f.part_stride + (int64_t)chunk * a.np;
         for (int k = tid; k < a.np; k += kThreads) {
             float sx = 0.f, sy = 0.f;
 #pragma unroll 8
@@ -598,9 +538,9 @@ hs_pass_kernel(const PassArgs a)
             }
             out[k] = make_float2(sx, sy);
         }
-        if (a.u.act != ACT_NONE) {
+        if (a.f.u.act != ACT_NONE) {
             __syncthreads();
-            hs_fold(a, pat, chunk, reinterpret_cast<char *>(E_s));
+            hs_fold(a.f, pat, chunk, reinterpret_cast<char *>(E_s));
         }
     }
 }

@@ -21,6 +21,7 @@
 
 #include "../../include/holospots_b200.h"
 #include "hs_kernels.cuh"
+#include "hs_tile.cuh"
 
 using namespace hs;
 
@@ -76,24 +77,35 @@ void dfree(T *&p)
 }
 
 // G lanes per pixel, NL spots per lane (a template value), np = G * NL.
+// For n <= 128 the padded width is a multiple of 16 so the full-range passes
+// can use the GEMM-tile kernel (ns = np / 16 spots per forward lane).
 struct Config {
-    int G, NL, np, spw;
+    int G, NL, np, spw, ns;
 };
 
 Config pick_config(int n)
 {
     Config c{};
-    c.G = 1;
-    while (c.G < 32 && (n + c.G - 1) / c.G > 16) c.G *= 2;
-    int nl = (n + c.G - 1) / c.G;
-    nl += nl & 1;
     const int choices[] = {4, 8, 10, 12, 14, 16, 32};
-    for (int v : choices)
-        if (v >= nl) {
-            c.NL = v;
-            break;
-        }
-    c.np = c.G * c.NL;
+    if (n <= 128) {
+        c.np = 16 * ((n + 15) / 16);
+        c.ns = c.np / 16;
+        c.G = 1;
+        while (c.np / c.G > 16) c.G *= 2;
+        c.NL = c.np / c.G;
+    } else {
+        c.ns = 0;
+        c.G = 1;
+        while (c.G < 32 && (n + c.G - 1) / c.G > 16) c.G *= 2;
+        int nl = (n + c.G - 1) / c.G;
+        nl += nl & 1;
+        for (int v : choices)
+            if (v >= nl) {
+                c.NL = v;
+                break;
+            }
+        c.np = c.G * c.NL;
+    }
     c.spw = 32 / c.G;
     return c;
 }
@@ -125,6 +137,10 @@ struct hs_plan {
     std::vector<int32_t> h_index;  // grid -> storage index, -1 outside
     std::vector<int32_t> row_lo, row_hi;
     double *d_axis = nullptr;
+    float *d_amp_img = nullptr;           // [side][side] amplitude, 0 outside
+    int32_t *d_idx_img = nullptr;         // [side][side] storage index, -1 outside
+    int32_t *d_tiles = nullptr;           // non-empty 64x32 tiles, packed (r0 << 16) | c0
+    int32_t ntiles = 0;
     DevList storage;                      // storage order
     std::map<int, DevList> dense;         // full range, banded layout per slots-per-warp
     std::map<std::pair<int64_t, int64_t>, DevList> windows;  // sorted (row, col)
@@ -412,6 +428,48 @@ int launch_tables(hs_plan *p, bool seed)
     return HS_OK;
 }
 
+FoldArgs fold_args(hs_plan *p, int32_t nchunks, const UpdArgs &u)
+{
+    FoldArgs f;
+    f.nchunks = nchunks;
+    f.np = p->cfg.np;
+    f.partials = p->d_part;
+    f.part_stride = p->part_stride;
+    f.gpart = p->d_gpart;
+    f.gpart_stride = p->gpart_stride;
+    f.grp_cnt = p->d_grp_cnt;
+    f.pat_cnt = p->d_pat_cnt;
+    f.cnt_stride = p->cnt_stride;
+    f.u = u;
+    return f;
+}
+
+// Full-range fused pass with the GEMM-tile kernel (n <= 128).
+int launch_tile(hs_plan *p, bool write, const UpdArgs &u)
+{
+    const Config &c = p->cfg;
+    if (p->ntiles > p->cap_chunks) return fail(HS_ECUDA, "fold buffers too small (%d tiles)", p->ntiles);
+    TileArgs a;
+    memset(&a, 0, sizeof a);
+    a.tiles = p->d_tiles;
+    a.side = p->side;
+    a.np = c.np;
+    a.tab_stride = (int64_t)p->side * c.np;
+    a.gx = p->d_gx;
+    a.gy = p->d_gy;
+    a.coef = p->d_coef;
+    a.amp_img = p->d_amp_img;
+    a.idx_img = p->d_idx_img;
+    a.phase_out = p->d_phase;
+    a.phase_stride = p->m;
+    a.f = fold_args(p, p->ntiles, u);
+    TileFn fn = hs_select_tile(c.ns, write);
+    dim3 grid(p->ntiles, p->batch);
+    fn<<<grid, kThreads, hs_tile_smem_bytes(c.ns), p->stream>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    return HS_OK;
+}
+
 // One pass over `count` entries of list `l` starting at entry `off`.
 int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t count, int64_t idx_base,
                 const double *phase_in, double *phase_out, int64_t phase_stride, const UpdArgs &u)
@@ -428,7 +486,6 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
     a.idx_base = idx_base;
     a.count = count;
     a.chunk_len = geo.chunk_len;
-    a.nchunks = geo.nchunks;
     a.np = c.np;
     a.nl = c.NL;
     a.sorted_rows = l.sorted_rows;
@@ -439,14 +496,7 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
     a.phase_in = phase_in;
     a.phase_out = phase_out;
     a.phase_stride = phase_stride;
-    a.partials = p->d_part;
-    a.part_stride = p->part_stride;
-    a.gpart = p->d_gpart;
-    a.gpart_stride = p->gpart_stride;
-    a.grp_cnt = p->d_grp_cnt;
-    a.pat_cnt = p->d_pat_cnt;
-    a.cnt_stride = p->cnt_stride;
-    a.u = u;
+    a.f = fold_args(p, geo.nchunks, u);
     PassFn fn = select_pass(c, mode);
     dim3 grid(geo.nchunks, p->batch);
     fn<<<grid, kThreads, pass_smem(c), p->stream>>>(a);
@@ -487,25 +537,34 @@ int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags)
     if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
     const int final_mode = want_fields ? (PM_BWD | PM_FWD | PM_WRITE) : (PM_BWD | PM_WRITE);
     const UpdArgs fin = upd_args(p, want_fields ? ACT_FINAL : ACT_NONE);
-    if (alg == HS_ALG_RS)
-        return launch_pass(p, final_mode, *dense, 0, dense->count, 0, nullptr, p->d_phase, m, fin);
+    const bool tiled = p->cfg.ns > 0;
+    auto full_pass = [&](int mode, const UpdArgs &u) -> int {
+        if (tiled && (mode & PM_FWD)) return launch_tile(p, (mode & PM_WRITE) != 0, u);
+        return launch_pass(p, mode, *dense, 0, dense->count, 0, nullptr, (mode & PM_WRITE) ? p->d_phase : nullptr,
+                           m, u);
+    };
+    if (alg == HS_ALG_RS) return full_pass(final_mode, fin);
     const int cs = (subset < m) ? std::max(0, iters - 2) : 0;
     const int64_t half = std::max<int64_t>(1, subset / 2);
     for (int j = 0; j <= iters; ++j) {
         // list of pass j: read_1 for j = 0, write_j otherwise
-        const DevList *lst = dense;
+        const DevList *lst = nullptr;
         if (j == 0 ? cs > 0 : j <= cs) {
             const int64_t off = (j == 0) ? 0 : ((int64_t)(j - 1) * half) % (m - subset + 1);
             if ((rc = get_window(p, off, subset, &lst))) return rc;
         }
+        UpdArgs u = fin;
+        int mode = final_mode;
         if (j < iters) {
-            UpdArgs u = upd_args(p, ACT_STEP);
+            u = upd_args(p, ACT_STEP);
             u.iter = j;
             u.iters = iters;
-            rc = launch_pass(p, PM_BWD | PM_FWD, *lst, 0, lst->count, 0, nullptr, nullptr, 0, u);
-        } else {
-            rc = launch_pass(p, final_mode, *lst, 0, lst->count, 0, nullptr, p->d_phase, m, fin);
+            mode = PM_BWD | PM_FWD;
         }
+        if (lst)
+            rc = launch_pass(p, mode, *lst, 0, lst->count, 0, nullptr, nullptr, 0, u);
+        else
+            rc = full_pass(mode, u);
         if (rc) return rc;
     }
     return HS_OK;
@@ -582,13 +641,38 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
     if ((rc = dalloc(&p->d_axis, side))) return rc;
     CUDA_TRY(cudaMemcpy(p->d_axis, axis, sizeof(double) * side, cudaMemcpyHostToDevice));
     if ((rc = build_storage(p.get()))) return rc;
+    {
+        const size_t cells = (size_t)side * side;
+        std::vector<float> amp_img(cells, 0.f);
+        for (int64_t i = 0; i < m; ++i) amp_img[(size_t)p->h_rows[i] * side + p->h_cols[i]] = p->h_amp[i];
+        std::vector<int32_t> tiles;
+        for (int r0 = 0; r0 < side; r0 += kTileR)
+            for (int c0 = 0; c0 < side; c0 += kTileC) {
+                bool any = false;
+                for (int r = r0; r < std::min(r0 + kTileR, side) && !any; ++r)
+                    any = p->row_lo[r] < std::min(c0 + kTileC, side) && p->row_hi[r] > c0;
+                if (any) tiles.push_back((r0 << 16) | c0);
+            }
+        p->ntiles = (int32_t)tiles.size();
+        if ((rc = dalloc(&p->d_amp_img, cells)) || (rc = dalloc(&p->d_idx_img, cells)) ||
+            (rc = dalloc(&p->d_tiles, tiles.size())))
+            return rc;
+        CUDA_TRY(cudaMemcpy(p->d_amp_img, amp_img.data(), cells * sizeof(float), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(p->d_idx_img, p->h_index.data(), cells * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        for (int ns = 1; ns <= 8; ++ns)
+            for (int w = 0; w < 2; ++w)
+                CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_tile(ns, w != 0),
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)hs_tile_smem_bytes(ns)));
+    }
     const int modes[4] = {PM_BWD | PM_WRITE, PM_FWD, PM_BWD | PM_FWD, PM_BWD | PM_FWD | PM_WRITE};
     const int gs[6] = {1, 2, 4, 8, 16, 32};
     const int nls[7] = {4, 8, 10, 12, 14, 16, 32};
     for (int G : gs)
         for (int NL : nls) {
             if (NL == 32 && G != 32) continue;
-            Config c{G, NL, G * NL, 32 / G};
+            Config c{G, NL, G * NL, 32 / G, 0};
             for (int mode : modes)
                 CUDA_TRY(cudaFuncSetAttribute((const void *)select_pass(c, mode),
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(c)));
@@ -607,6 +691,9 @@ void hs_plan_destroy(hs_plan *p)
     for (auto &kv : p->dense) free_list(kv.second);
     for (auto &kv : p->windows) free_list(kv.second);
     dfree(p->d_axis);
+    dfree(p->d_amp_img);
+    dfree(p->d_idx_img);
+    dfree(p->d_tiles);
     cudaStreamDestroy(p->stream);
     delete p;
 }
@@ -626,7 +713,8 @@ int hs_set_spots(hs_plan *p, int batch, int n, const double *x, const double *y,
     const DevList *dense;
     if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
     const int64_t chunks = std::max<int64_t>({(int64_t)geom_of(*dense, dense->count, p->cfg.spw).nchunks,
-                                              (int64_t)kTargetChunks + 1, p->m / kMaxChunk + 2});
+                                              (int64_t)kTargetChunks + 1, p->m / kMaxChunk + 2,
+                                              (int64_t)p->ntiles});
     if ((rc = ensure_fold(p, chunks))) return rc;
     const size_t bytes = sizeof(double) * (size_t)batch * n;
     CUDA_TRY(cudaMemcpyAsync(p->d_x, x, bytes, cudaMemcpyHostToDevice, p->stream));
@@ -894,12 +982,14 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
     CUDA_TRY(cudaEventCreate(&e0));
     CUDA_TRY(cudaEventCreate(&e1));
     const UpdArgs u = upd_args(p, ACT_FIELDS);
-    if ((rc = reset_status(p)) ||
-        (rc = launch_pass(p, PM_BWD | PM_FWD, *l, 0, l->count, 0, nullptr, nullptr, 0, u)))
-        return rc;
+    auto once = [&]() -> int {
+        if (which == 0 && p->cfg.ns > 0) return launch_tile(p, false, u);
+        return launch_pass(p, PM_BWD | PM_FWD, *l, 0, l->count, 0, nullptr, nullptr, 0, u);
+    };
+    if ((rc = reset_status(p)) || (rc = once())) return rc;
     CUDA_TRY(cudaEventRecord(e0, p->stream));
     for (int r = 0; r < reps; ++r)
-        if ((rc = launch_pass(p, PM_BWD | PM_FWD, *l, 0, l->count, 0, nullptr, nullptr, 0, u))) return rc;
+        if ((rc = once())) return rc;
     CUDA_TRY(cudaEventRecord(e1, p->stream));
     CUDA_TRY(cudaEventSynchronize(e1));
     float ms = 0.f;
