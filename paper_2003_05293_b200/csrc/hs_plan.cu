@@ -22,6 +22,7 @@
 #include "../../include/holospots_b200.h"
 #include "hs_kernels.cuh"
 #include "hs_tile.cuh"
+#include "hs_win.cuh"
 
 using namespace hs;
 
@@ -497,9 +498,14 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
     a.phase_out = phase_out;
     a.phase_stride = phase_stride;
     a.f = fold_args(p, geo.nchunks, u);
-    PassFn fn = select_pass(c, mode);
     dim3 grid(geo.nchunks, p->batch);
-    fn<<<grid, kThreads, pass_smem(c), p->stream>>>(a);
+    if (l.sorted_rows && c.ns > 0 && mode == (PM_BWD | PM_FWD)) {
+        // compressed window: latency-shaped kernel (16 lanes per pixel)
+        hs_select_win(c.ns)<<<grid, kThreads, hs_win_smem_bytes(c.ns), p->stream>>>(a);
+    } else {
+        PassFn fn = select_pass(c, mode);
+        fn<<<grid, kThreads, pass_smem(c), p->stream>>>(a);
+    }
     CUDA_TRY(cudaGetLastError());
     return HS_OK;
 }
