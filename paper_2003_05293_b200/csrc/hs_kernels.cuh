@@ -83,7 +83,8 @@ struct PassArgs {
     int64_t count;            // list length
     int32_t chunk_len;        // entries per CTA; multiple of 8 * SPW
     int32_t np, nl;           // padded spot count, spots per lane (even)
-    int32_t sorted_rows;      // list is sorted by row (window lists): stage gy rows
+    int32_t sorted_rows;      // list is sorted by row (window lists)
+    int32_t cpc;              // logical chunks per CTA (divides kGroup; window kernel)
     int64_t tab_stride;       // side * np
     const float2 *gx, *gy;    // [B][side][np]
     const float2 *coef;       // [B][np]
@@ -283,7 +284,7 @@ __device__ __forceinline__ void hs_update(const UpdArgs &a, int b, double2 *E, d
 // of each kGroup-chunk group folds the group in chunk order (fp64); the last
 // group-folder of the pattern folds the groups in order and applies the
 // action.  Counters reset themselves, so graphs replay without memsets.
-__device__ __forceinline__ void hs_fold(const FoldArgs &a, int pat, int chunk, char *scratch)
+__device__ __forceinline__ void hs_fold(const FoldArgs &a, int pat, int chunk, char *scratch, int arrivals = 1)
 {
     __shared__ int s_last;
     __shared__ double dbuf[kThreads];
@@ -297,8 +298,8 @@ __device__ __forceinline__ void hs_fold(const FoldArgs &a, int pat, int chunk, c
     __threadfence();
     __syncthreads();
     if (tid == 0) {
-        const int t = atomicAdd(a.grp_cnt + (int64_t)pat * a.cnt_stride + grp, 1);
-        s_last = (t == c1 - c0 - 1);
+        const int t = atomicAdd(a.grp_cnt + (int64_t)pat * a.cnt_stride + grp, arrivals);
+        s_last = (t + arrivals == c1 - c0);
     }
     __syncthreads();
     if (!s_last) return;

@@ -500,7 +500,12 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
     a.f = fold_args(p, geo.nchunks, u);
     dim3 grid(geo.nchunks, p->batch);
     if (l.sorted_rows && c.ns > 0 && mode == (PM_BWD | PM_FWD)) {
-        // compressed window: latency-shaped kernel (16 lanes per pixel)
+        // compressed window: latency-shaped kernel (16 lanes per pixel); a
+        // CTA streams cpc logical chunks when the batch gives enough CTAs
+        int cpc = 1;
+        while (cpc < kMaxCpc && (int64_t)geo.nchunks * p->batch / (2 * cpc) >= 4 * kTargetChunks) cpc *= 2;
+        a.cpc = cpc;
+        grid.x = (geo.nchunks + cpc - 1) / cpc;
         hs_select_win(c.ns)<<<grid, kThreads, hs_win_smem_bytes(c.ns), p->stream>>>(a);
     } else {
         PassFn fn = select_pass(c, mode);
@@ -666,6 +671,9 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
         CUDA_TRY(cudaMemcpy(p->d_amp_img, amp_img.data(), cells * sizeof(float), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(p->d_idx_img, p->h_index.data(), cells * sizeof(int32_t), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        for (int ns = 1; ns <= 8; ++ns)
+            CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_win(ns), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)hs_win_smem_bytes(ns)));
         for (int ns = 1; ns <= 8; ++ns)
             for (int w = 0; w < 2; ++w)
                 CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_tile(ns, w != 0),

@@ -21,11 +21,17 @@
 
 namespace hs {
 
+constexpr int kMaxCpc = 8;  // logical chunks per CTA (divides kGroup)
+
 __host__ __device__ constexpr size_t hs_win_smem_bytes(int NL)
 {
-    return sizeof(float2) * (size_t)16 * NL * (1 + kWarps);
+    return sizeof(float2) * (size_t)16 * NL * (1 + kMaxCpc * kWarps);
 }
 
+// One CTA streams `cpc` consecutive logical chunks (a.cpc) of one pattern.
+// Each logical chunk keeps its own fixed warp segmentation and its own
+// partial, so results do not depend on cpc; the gx prefetch pipeline runs
+// across chunk boundaries.
 template <int NL>
 __global__ void __launch_bounds__(kThreads, 2) hs_win_kernel(const PassArgs a)
 {
@@ -34,11 +40,12 @@ __global__ void __launch_bounds__(kThreads, 2) hs_win_kernel(const PassArgs a)
     constexpr int NP = G * NL;
     extern __shared__ float2 smw[];
     float2 *coef_s = smw;           // [NP]
-    float2 *Ew = smw + NP;          // [kWarps][NP]
+    float2 *Ew = smw + NP;          // [cpc][kWarps][NP]
 
     const int pat = blockIdx.y;
-    const int chunk = blockIdx.x;
     if (a.f.u.status[pat] != 0) return;
+    const int q0 = blockIdx.x * a.cpc;
+    const int nq = min(a.cpc, a.f.nchunks - q0);
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int g = lane & (G - 1), s = lane / G;
@@ -48,12 +55,10 @@ __global__ void __launch_bounds__(kThreads, 2) hs_win_kernel(const PassArgs a)
 
     const float2 *__restrict__ X = a.gx + (int64_t)pat * a.tab_stride + g;
     const float2 *__restrict__ Y = a.gy + (int64_t)pat * a.tab_stride + g;
-    const int64_t begin = (int64_t)chunk * a.chunk_len;
     const int wseg = a.chunk_len / kWarps;
-    const int64_t wb = begin + (int64_t)warp * wseg;
-    int64_t we = wb + wseg;
-    if (we > a.count) we = a.count;
-    const int trips = (we > wb) ? (int)((we - wb + SPW - 1) / SPW) : 0;
+    const int tf = wseg / SPW;                // trips per logical chunk
+    const int total = nq * tf;
+    const int64_t wbase = (int64_t)q0 * a.chunk_len + (int64_t)warp * wseg + s;
 
     float vr[NL], vi[NL], tr[NL], ti[NL], er[NL], ei[NL], xr[NL], xi[NL], nr[NL], ni[NL];
 #pragma unroll
@@ -61,14 +66,17 @@ __global__ void __launch_bounds__(kThreads, 2) hs_win_kernel(const PassArgs a)
         vr[j] = vi[j] = tr[j] = ti[j] = er[j] = ei[j] = 0.f;
         xr[j] = xi[j] = nr[j] = ni[j] = 0.f;
     }
-    auto entry = [&](int t, int &rc, float &A) {
-        const int64_t i = wb + (int64_t)t * SPW + s;
-        if (t < trips && i < we) {
-            rc = __ldg(a.rc + i);
-            A = __ldg(a.amp + i);
-        } else {
-            rc = -1;
-            A = 0.f;
+    // flattened trip T -> (chunk q = T / tf, trip t = T % tf)
+    auto entry = [&](int T, int &rc, float &A) {
+        rc = -1;
+        A = 0.f;
+        if (T < total) {
+            const int q = T / tf, t = T - q * tf;
+            const int64_t i = wbase + (int64_t)q * a.chunk_len + (int64_t)t * SPW;
+            if (i < a.count) {
+                rc = __ldg(a.rc + i);
+                A = __ldg(a.amp + i);
+            }
         }
     };
     auto load_x = [&](int rc, float *dr, float *di) {
@@ -80,6 +88,19 @@ __global__ void __launch_bounds__(kThreads, 2) hs_win_kernel(const PassArgs a)
             di[j] = q.y;
         }
     };
+    auto flush = [&](int r) {  // E += gy[r] * T ; T = 0
+        const float2 *yr = Y + (int64_t)r * NP;
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            const float2 q = __ldg(yr + G * j);
+            er[j] = fmaf(q.x, tr[j], er[j]);
+            er[j] = fmaf(-q.y, ti[j], er[j]);
+            ei[j] = fmaf(q.x, ti[j], ei[j]);
+            ei[j] = fmaf(q.y, tr[j], ei[j]);
+            tr[j] = 0.f;
+            ti[j] = 0.f;
+        }
+    };
 
     int rc_c, rc_n;
     float A_c, A_n;
@@ -88,28 +109,16 @@ __global__ void __launch_bounds__(kThreads, 2) hs_win_kernel(const PassArgs a)
     load_x(rc_c, xr, xi);
     int rcur = -1;
 
-    for (int t = 0; t < trips; ++t) {
-        // prefetch: next pixel's gx row and the entry after it
-        load_x(rc_n, nr, ni);
+#pragma unroll 2
+    for (int T = 0; T < total; ++T) {
+        load_x(rc_n, nr, ni);                 // next pixel's gx row
         int rc_nn;
         float A_nn;
-        entry(t + 2, rc_nn, A_nn);
+        entry(T + 2, rc_nn, A_nn);
 
         const int r = rc_c < 0 ? rcur : (rc_c >> 16);
         if (r != rcur && r >= 0) {
-            if (rcur >= 0) {  // E += gy[rcur] * T ; T = 0
-                const float2 *yr = Y + (int64_t)rcur * NP;
-#pragma unroll
-                for (int j = 0; j < NL; ++j) {
-                    const float2 q = __ldg(yr + G * j);
-                    er[j] = fmaf(q.x, tr[j], er[j]);
-                    er[j] = fmaf(-q.y, ti[j], er[j]);
-                    ei[j] = fmaf(q.x, ti[j], ei[j]);
-                    ei[j] = fmaf(q.y, tr[j], ei[j]);
-                    tr[j] = 0.f;
-                    ti[j] = 0.f;
-                }
-            }
+            if (rcur >= 0) flush(rcur);
             const float2 *yr = Y + (int64_t)r * NP;
 #pragma unroll
             for (int j = 0; j < NL; ++j) {
@@ -171,40 +180,38 @@ __global__ void __launch_bounds__(kThreads, 2) hs_win_kernel(const PassArgs a)
         A_c = A_n;
         rc_n = rc_nn;
         A_n = A_nn;
-    }
-    if (rcur >= 0) {
-        const float2 *yr = Y + (int64_t)rcur * NP;
+
+        if ((T + 1) % tf == 0) {
+            // end of logical chunk q: its E, slots folded by one symmetric
+            // add, stored per warp; state restarts for the next chunk.
+            if (rcur >= 0) flush(rcur);
+            rcur = -1;
+            const int q = T / tf;
 #pragma unroll
-        for (int j = 0; j < NL; ++j) {
-            const float2 q = __ldg(yr + G * j);
-            er[j] = fmaf(q.x, tr[j], er[j]);
-            er[j] = fmaf(-q.y, ti[j], er[j]);
-            ei[j] = fmaf(q.x, ti[j], ei[j]);
-            ei[j] = fmaf(q.y, tr[j], ei[j]);
+            for (int j = 0; j < NL; ++j) {
+                const float ex = er[j] + __shfl_xor_sync(0xffffffffu, er[j], 16);
+                const float ey = ei[j] + __shfl_xor_sync(0xffffffffu, ei[j], 16);
+                if (s == 0) Ew[(q * kWarps + warp) * NP + g + G * j] = make_float2(ex, ey);
+                er[j] = 0.f;
+                ei[j] = 0.f;
+            }
         }
     }
-    // slots of the warp (lanes g and g+16): one symmetric add, then warps in order
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-        er[j] += __shfl_xor_sync(0xffffffffu, er[j], 16);
-        ei[j] += __shfl_xor_sync(0xffffffffu, ei[j], 16);
-        if (s == 0) Ew[warp * NP + g + G * j] = make_float2(er[j], ei[j]);
-    }
     __syncthreads();
-    float2 *out = a.f.partials + (int64_t)pat * a.f.part_stride + (int64_t)chunk * NP;
-    for (int k = tid; k < NP; k += kThreads) {
+    for (int k = tid; k < nq * NP; k += kThreads) {
+        const int q = k / NP, n = k - q * NP;
         float x = 0.f, y = 0.f;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-            const float2 v = Ew[w * NP + k];
+            const float2 v = Ew[(q * kWarps + w) * NP + n];
             x += v.x;
             y += v.y;
         }
-        out[k] = make_float2(x, y);
+        a.f.partials[(int64_t)pat * a.f.part_stride + (int64_t)(q0 + q) * NP + n] = make_float2(x, y);
     }
     if (a.f.u.act != ACT_NONE) {
         __syncthreads();
-        hs_fold(a.f, pat, chunk, reinterpret_cast<char *>(smw));
+        hs_fold(a.f, pat, q0, reinterpret_cast<char *>(smw), nq);
     }
 }
 
