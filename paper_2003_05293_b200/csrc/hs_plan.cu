@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -142,6 +143,7 @@ struct hs_plan {
     int32_t *d_idx_img = nullptr;         // [side][side] storage index, -1 outside
     int32_t *d_tiles = nullptr;           // non-empty 64x32 tiles, packed (r0 << 16) | c0
     int32_t ntiles = 0;
+    int win_minb = 2;                     // resident CTAs/SM the window kernel is built for
     DevList storage;                      // storage order
     std::map<int, DevList> dense;         // full range, banded layout per slots-per-warp
     std::map<std::pair<int64_t, int64_t>, DevList> windows;  // sorted (row, col)
@@ -506,7 +508,7 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
         while (cpc < kMaxCpc && (int64_t)geo.nchunks * p->batch / (2 * cpc) >= 4 * kTargetChunks) cpc *= 2;
         a.cpc = cpc;
         grid.x = (geo.nchunks + cpc - 1) / cpc;
-        hs_select_win(c.ns)<<<grid, kThreads, hs_win_smem_bytes(c.ns), p->stream>>>(a);
+        hs_select_win(c.ns, p->win_minb)<<<grid, kThreads, hs_win_smem_bytes(c.ns), p->stream>>>(a);
     } else {
         PassFn fn = select_pass(c, mode);
         fn<<<grid, kThreads, pass_smem(c), p->stream>>>(a);
@@ -671,9 +673,11 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
         CUDA_TRY(cudaMemcpy(p->d_amp_img, amp_img.data(), cells * sizeof(float), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(p->d_idx_img, p->h_index.data(), cells * sizeof(int32_t), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        if (const char *env = getenv("HS_WIN_MINB")) p->win_minb = atoi(env);
         for (int ns = 1; ns <= 8; ++ns)
-            CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_win(ns), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)hs_win_smem_bytes(ns)));
+            for (int mb = 2; mb <= 4; ++mb)
+                CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_win(ns, mb),
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs_win_smem_bytes(ns)));
         for (int ns = 1; ns <= 8; ++ns)
             for (int w = 0; w < 2; ++w)
                 CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_tile(ns, w != 0),

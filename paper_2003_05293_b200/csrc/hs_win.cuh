@@ -21,7 +21,7 @@
 
 namespace hs {
 
-constexpr int kMaxCpc = 8;  // logical chunks per CTA (divides kGroup)
+constexpr int kMaxCpc = 4;  // logical chunks per CTA (divides kGroup)
 
 __host__ __device__ constexpr size_t hs_win_smem_bytes(int NL)
 {
@@ -32,8 +32,8 @@ __host__ __device__ constexpr size_t hs_win_smem_bytes(int NL)
 // Each logical chunk keeps its own fixed warp segmentation and its own
 // partial, so results do not depend on cpc; the gx prefetch pipeline runs
 // across chunk boundaries.
-template <int NL>
-__global__ void __launch_bounds__(kThreads, 2) hs_win_kernel(const PassArgs a)
+template <int NL, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) hs_win_kernel(const PassArgs a)
 {
     constexpr int G = 16;
     constexpr int SPW = 32 / G;
@@ -216,6 +216,6 @@ __global__ void __launch_bounds__(kThreads, 2) hs_win_kernel(const PassArgs a)
 }
 
 typedef void (*WinFn)(PassArgs);
-WinFn hs_select_win(int nl);
+WinFn hs_select_win(int nl, int minb = 2);
 
 }  // namespace hs

@@ -1,0 +1,81 @@
+"""Multi-GPU sharding logic (one process per GPU).
+
+Two decompositions:
+
+* **Batch data parallelism** (configs 3 / 5): independent patterns are split
+  into contiguous per-rank ranges. There is no data-path collective; each
+  rank owns its own plan and device.
+* **Pixel sharding of one hologram** (config 4): the fixed chunk list of a
+  pass (tiles for full-range passes, sorted-window chunks for compressed
+  ones) is split across ranks **at fold-group boundaries** (groups of
+  ``GROUP`` chunks, the first level of the device fold tree,
+  csrc/hs_kernels.cuh ``kGroup``). Every group is then folded by exactly one
+  rank, in the device order. The exchange is an all-gather of the
+  ``ngroups x np`` complex128 group partials. Every rank folds them in group
+  order, so the fields are bitwise identical on every rank and identical to
+  the single-GPU result for any world size.
+
+``fold_groups`` / ``fold_fields`` restate the device fold on the host so the
+gloo tests can check the invariance without a GPU.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+GROUP = 32  # chunks per first-level fold group (kGroup in hs_kernels.cuh)
+
+
+def shard_patterns(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous pattern range [first, first + count) of ``rank``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("invalid rank / world")
+    base, extra = divmod(total, world)
+    first = rank * base + min(rank, extra)
+    return first, base + (1 if rank < extra else 0)
+
+
+def shard_groups(nchunks: int, world: int) -> list[tuple[int, int]]:
+    """Per-rank chunk ranges aligned to fold groups, balanced by chunk count."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    ngroups = -(-nchunks // GROUP)
+    bounds = []
+    for r in range(world + 1):
+        g = (r * ngroups) // world
+        bounds.append(min(g * GROUP, nchunks))
+    return [(bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+def fold_groups(partials: np.ndarray, lo: int, hi: int) -> np.ndarray:
+    """Group partials of chunks [lo, hi) (group-aligned): fp64 sums of the
+    fp32 chunk partials in chunk order, one row per group."""
+    part = np.asarray(partials)
+    out = []
+    for g0 in range(lo, hi, GROUP):
+        acc = np.zeros(part.shape[1], dtype=np.complex128)
+        for c in range(g0, min(g0 + GROUP, hi)):
+            acc = acc + part[c].astype(np.complex128)
+        out.append(acc)
+    return np.array(out).reshape(-1, part.shape[1])
+
+
+def fold_fields(group_partials: np.ndarray) -> np.ndarray:
+    """Second fold level: groups summed in group order (fp64)."""
+    acc = np.zeros(group_partials.shape[1], dtype=np.complex128)
+    for row in group_partials:
+        acc = acc + row
+    return acc
+
+
+def sharded_fields(partials: np.ndarray, world: int, rank: int, all_gather) -> np.ndarray:
+    """Fields of one pass computed by ``world`` ranks.
+
+    Rank ``rank`` folds its groups, ``all_gather(local) -> list`` exchanges
+    the group partials (rank order = group order), and every rank folds the
+    same sequence.
+    """
+    lo, hi = shard_groups(partials.shape[0], world)[rank]
+    local = fold_groups(partials, lo, hi)
+    gathered = all_gather(local)
+    return fold_fields(np.concatenate([g for g in gathered if g.size], axis=0))
