@@ -101,6 +101,14 @@ int hs_forward(hs_plan *plan, const double *phase, int64_t start, int64_t stop,
 int hs_quality(hs_plan *plan, const double *phase, double *e, double *u,
                double *intensities, double *relative, double *fields);
 
+/* Far-field probe intensities (simulate.py:48-63): |E|^2 / (sum A)^2 of the
+ * hologram phase[m] at npts probe positions xyz[npts][3], evaluated in
+ * chunks of `batch` probes with the same kernels and normalisation as
+ * hs_quality (a probe on a target spot reproduces its intensity bit for
+ * bit).  Replaces the plan's current spot set. */
+int hs_probe(hs_plan *plan, const double *phase, int64_t npts, const double *xyz,
+             int batch, double *out);
+
 /* Run `algorithm` on all patterns of the current spot batch.
  * iterations: I (ignored for RS); subset: ceil(c*M) for CS-WGS (M for WGS);
  * theta0: [batch][n] starting phase offsets (solvers.py:169-170).

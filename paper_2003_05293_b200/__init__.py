@@ -20,6 +20,7 @@ from .optics import (CompressionPlan, Hologram, Pupil, SpotSet, build_pupil, pha
 from .solvers import (PlannedRun, SolverConfig, SolverTrace, StepRecord, WgsState,
                       budget_controller, cswgs, predict_ops, rebalance_weights, rs, solve,
                       solve_batch, wgs, wgs_step)
+from .simulate import FieldImage, probe_intensities, render_plane
 from ._lib import get_device, set_device
 from .workloads import grid_spots, named_spots, random_foci
 

@@ -42,7 +42,7 @@ EXPORTS = (
     "hs_solve_async", "hs_solve", "hs_sync", "hs_get_status", "hs_get_trace",
     "hs_get_phase", "hs_get_quality", "hs_solve_host", "hs_plan_stream",
     "hs_last_launch_count", "hs_time_kernel", "hs_fma_peak", "hs_host_alloc",
-    "hs_host_free",
+    "hs_host_free", "hs_probe",
 )
 
 _lib = None
@@ -84,6 +84,7 @@ def load():
             "hs_last_launch_count": (I, [P, ctypes.POINTER(I64)]),
             "hs_time_kernel": (I, [P, I, I64, I, ctypes.POINTER(D), ctypes.POINTER(D)]),
             "hs_fma_peak": (I, [I, ctypes.POINTER(D)]),
+            "hs_probe": (I, [P, P, I64, P, I, P]),
             "hs_host_alloc": (P, [I64]),
             "hs_host_free": (None, [P]),
         }
@@ -237,6 +238,16 @@ class Plan:
         check(load().hs_get_quality(self.handle, ptr(e), ptr(u), ptr(inten), ptr(rel),
                                     ptr(fields)))
         return e, u, inten, rel, fields[:, 0::2] + 1j * fields[:, 1::2]
+
+    def probe(self, phase, points, batch: int = 1024) -> np.ndarray:
+        pts = f64(np.atleast_2d(points))
+        out = np.empty(pts.shape[0], dtype=np.float64)
+        try:
+            check(load().hs_probe(self.handle, ptr(f64(phase)), pts.shape[0], ptr(pts),
+                                  int(batch), ptr(out)))
+        finally:
+            self._spots_key = None  # hs_probe replaced the device spot set
+        return out
 
     def stream(self) -> int:
         return int(load().hs_plan_stream(self.handle) or 0)

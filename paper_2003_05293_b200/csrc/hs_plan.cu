@@ -835,6 +835,39 @@ int hs_quality(hs_plan *p, const double *phase, double *e, double *u, double *in
     return HS_OK;
 }
 
+int hs_probe(hs_plan *p, const double *phase, int64_t npts, const double *xyz, int batch, double *out)
+{
+    if (!(p->sum_amp > 0.0)) return fail(HS_EZEROILLUM, "pupil carries no illumination");
+    if (batch < 1 || batch > hs_max_spots()) return fail(HS_EINVAL, "probe batch %d outside 1..%d", batch, hs_max_spots());
+    if (npts < 0) return fail(HS_EINVAL, "negative probe count");
+    int rc;
+    if ((rc = check_device(p))) return rc;
+    bool uploaded = false;
+    std::vector<double> x, y, z, a;
+    for (int64_t lo = 0; lo < npts; lo += batch) {
+        const int n = (int)std::min<int64_t>(batch, npts - lo);
+        x.resize(n); y.resize(n); z.resize(n); a.assign(n, 1.0);
+        for (int k = 0; k < n; ++k) {
+            x[k] = xyz[(lo + k) * 3 + 0];
+            y[k] = xyz[(lo + k) * 3 + 1];
+            z[k] = xyz[(lo + k) * 3 + 2];
+        }
+        if ((rc = hs_set_spots(p, 1, n, x.data(), y.data(), z.data(), a.data())) || (rc = ensure_tables(p)) ||
+            (rc = reset_status(p)))
+            return rc;
+        if (!uploaded) {
+            CUDA_TRY(cudaMemcpyAsync(p->d_phase, phase, sizeof(double) * p->m, cudaMemcpyHostToDevice, p->stream));
+            uploaded = true;
+        }
+        const DevList *dense;
+        if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
+        rc = launch_pass(p, PM_FWD, *dense, 0, dense->count, 0, p->d_phase, nullptr, 0, upd_args(p, ACT_FINAL));
+        if (rc) return rc;
+        CUDA_TRY(cudaMemcpyAsync(out + lo, p->d_inten, sizeof(double) * n, cudaMemcpyDeviceToHost, p->stream));
+    }
+    return sync_and_check(p);
+}
+
 int hs_solve_async(hs_plan *p, int alg, int iters, int64_t subset, const double *theta0, int flags)
 {
     if (p->batch < 1) return fail(HS_EINVAL, "no spots set");

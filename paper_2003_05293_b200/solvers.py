@@ -78,6 +78,9 @@ class SolverTrace:
     wall_time_s: float
     degenerate: bool
     hologram: Hologram
+    # extension: e/u of the final fused pass (QualityReport), computed on the
+    # device with no extra projection; quality_report() re-projects instead
+    quality: object = None
 
 
 @dataclass(frozen=True)
@@ -173,10 +176,11 @@ def _assemble(algorithm: str, pupil: Pupil, spots: SpotSet, res: BatchResult, b:
     _raise_status(int(res.status[b]))
     m, n = pupil.active_count, spots.count
     holo = Hologram(res.phases[b], pupil)
-    holo._fields = (spots, res.fields[b], res.efficiency[b], res.uniformity[b],
-                    res.intensities[b], res.relative[b])
+    from .metrics import QualityReport
+    fused = QualityReport(efficiency=float(res.efficiency[b]), uniformity=float(res.uniformity[b]),
+                          intensities=res.intensities[b].copy(), target_relative=res.relative[b].copy())
     if algorithm == "rs":
-        trace = SolverTrace("rs", (), m * n, time.perf_counter() - t0, False, holo)
+        trace = SolverTrace("rs", (), m * n, time.perf_counter() - t0, False, holo, fused)
         return holo, trace
     records, ops = [], 0
     first_deg = int(res.first_degenerate[b])
@@ -187,7 +191,7 @@ def _assemble(algorithm: str, pupil: Pupil, spots: SpotSet, res: BatchResult, b:
                                   subset_size=size, ops=ops,
                                   degenerate=bool(first_deg and j >= first_deg)))
     trace = SolverTrace(algorithm, tuple(records), ops, time.perf_counter() - t0,
-                        bool(first_deg), holo)
+                        bool(first_deg), holo, fused)
     return holo, trace
 
 

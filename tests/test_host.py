@@ -220,3 +220,18 @@ def test_reduce_complex_matches_golden(golden):
     assert hs.reduce_complex([1, 2, 3, 4], chunk=2) == 10
     with pytest.raises(hs.InvalidParameterError):
         hs.reduce_complex([1j], chunk=0)
+
+
+# ---------------------------------------------------------------- renderer
+def test_render_validation_before_device(pupils):
+    p = pupils["p8u1"]
+    holo = hs.Hologram(np.zeros(p.active_count), p)
+    with pytest.raises(hs.InvalidParameterError):
+        hs.render_plane(p, holo, window=1e-4, exposure="three_photon")
+    with pytest.raises(hs.InvalidParameterError):
+        hs.render_plane(p, holo, window=1e-4, resolution=0)
+    with pytest.raises(hs.InvalidParameterError):
+        hs.render_plane(p, holo, window=-1.0)
+    with pytest.raises(hs.InvalidParameterError):
+        hs.probe_intensities(p, holo, np.zeros((3, 2)))
+    assert hs.probe_intensities(p, holo, np.zeros((0, 3))).shape == (0,)
