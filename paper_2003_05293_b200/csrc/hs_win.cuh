@@ -66,21 +66,27 @@ __global__ void __launch_bounds__(kThreads, MINB) hs_win_kernel(const PassArgs a
         vr[j] = vi[j] = tr[j] = ti[j] = er[j] = ei[j] = 0.f;
         xr[j] = xi[j] = nr[j] = ni[j] = 0.f;
     }
-    // flattened trip T -> (chunk q = T / tf, trip t = T % tf)
-    auto entry = [&](int T, int &rc, float &A) {
+    // Entry stream (runs two trips ahead of the compute): chunk counter qe,
+    // trip-in-chunk te and list index ie advance incrementally.
+    int qe = 0, te = 0;
+    int64_t ie = wbase;
+    const int64_t wrap = (int64_t)a.chunk_len - (int64_t)wseg;
+    auto next_entry = [&](int &rc, float &A) {
         rc = -1;
         A = 0.f;
-        if (T < total) {
-            const int q = T / tf, t = T - q * tf;
-            const int64_t i = wbase + (int64_t)q * a.chunk_len + (int64_t)t * SPW;
-            if (i < a.count) {
-                rc = __ldg(a.rc + i);
-                A = __ldg(a.amp + i);
-            }
+        if (qe < nq && ie < a.count) {
+            rc = __ldg(a.rc + ie);
+            A = __ldg(a.amp + ie);
+        }
+        ie += SPW;
+        if (++te == tf) {
+            te = 0;
+            ++qe;
+            ie += wrap;
         }
     };
-    auto load_x = [&](int rc, float *dr, float *di) {
-        const float2 *xc = X + (int64_t)(rc < 0 ? 0 : (rc & 0xffff)) * NP;
+    auto load_x = [&](int rc, float (&dr)[NL], float (&di)[NL]) {
+        const float2 *xc = X + (rc < 0 ? 0 : (rc & 0xffff)) * NP;
 #pragma unroll
         for (int j = 0; j < NL; ++j) {
             const float2 q = __ldg(xc + G * j);
@@ -89,7 +95,7 @@ __global__ void __launch_bounds__(kThreads, MINB) hs_win_kernel(const PassArgs a
         }
     };
     auto flush = [&](int r) {  // E += gy[r] * T ; T = 0
-        const float2 *yr = Y + (int64_t)r * NP;
+        const float2 *yr = Y + r * NP;
 #pragma unroll
         for (int j = 0; j < NL; ++j) {
             const float2 q = __ldg(yr + G * j);
@@ -104,22 +110,24 @@ __global__ void __launch_bounds__(kThreads, MINB) hs_win_kernel(const PassArgs a
 
     int rc_c, rc_n;
     float A_c, A_n;
-    entry(0, rc_c, A_c);
-    entry(1, rc_n, A_n);
+    next_entry(rc_c, A_c);
+    next_entry(rc_n, A_n);
     load_x(rc_c, xr, xi);
-    int rcur = -1;
+    int rcur = -1, tc = 0, qc = 0;
 
-#pragma unroll 2
-    for (int T = 0; T < total; ++T) {
-        load_x(rc_n, nr, ni);                 // next pixel's gx row
+    // One trip: prefetch the next pixel's gx row into (pr, pi), compute the
+    // current pixel from (cr, ci).  Called with the two register sets
+    // swapped on alternate trips (no copies).
+    auto trip = [&](float (&cr)[NL], float (&ci)[NL], float (&pr)[NL], float (&pi)[NL]) {
+        load_x(rc_n, pr, pi);
         int rc_nn;
         float A_nn;
-        entry(T + 2, rc_nn, A_nn);
+        next_entry(rc_nn, A_nn);
 
         const int r = rc_c < 0 ? rcur : (rc_c >> 16);
         if (r != rcur && r >= 0) {
             if (rcur >= 0) flush(rcur);
-            const float2 *yr = Y + (int64_t)r * NP;
+            const float2 *yr = Y + r * NP;
 #pragma unroll
             for (int j = 0; j < NL; ++j) {
                 const float2 q = __ldg(yr + G * j);
@@ -129,20 +137,19 @@ __global__ void __launch_bounds__(kThreads, MINB) hs_win_kernel(const PassArgs a
             }
             rcur = r;
         }
-
         float s0r = 0.f, s0i = 0.f, s1r = 0.f, s1i = 0.f;
 #pragma unroll
         for (int j = 0; j < NL; ++j) {
             if (j & 1) {
-                s1r = fmaf(vr[j], xr[j], s1r);
-                s1r = fmaf(-vi[j], xi[j], s1r);
-                s1i = fmaf(vr[j], xi[j], s1i);
-                s1i = fmaf(vi[j], xr[j], s1i);
+                s1r = fmaf(vr[j], cr[j], s1r);
+                s1r = fmaf(-vi[j], ci[j], s1r);
+                s1i = fmaf(vr[j], ci[j], s1i);
+                s1i = fmaf(vi[j], cr[j], s1i);
             } else {
-                s0r = fmaf(vr[j], xr[j], s0r);
-                s0r = fmaf(-vi[j], xi[j], s0r);
-                s0i = fmaf(vr[j], xi[j], s0i);
-                s0i = fmaf(vi[j], xr[j], s0i);
+                s0r = fmaf(vr[j], cr[j], s0r);
+                s0r = fmaf(-vi[j], ci[j], s0r);
+                s0i = fmaf(vr[j], ci[j], s0i);
+                s0i = fmaf(vi[j], cr[j], s0i);
             }
         }
         float sr = s0r + s1r, si = s0i + s1i;
@@ -169,34 +176,40 @@ __global__ void __launch_bounds__(kThreads, MINB) hs_win_kernel(const PassArgs a
         }
 #pragma unroll
         for (int j = 0; j < NL; ++j) {
-            tr[j] = fmaf(br, xr[j], tr[j]);
-            tr[j] = fmaf(-bi, xi[j], tr[j]);
-            ti[j] = fmaf(br, xi[j], ti[j]);
-            ti[j] = fmaf(bi, xr[j], ti[j]);
-            xr[j] = nr[j];
-            xi[j] = ni[j];
+            tr[j] = fmaf(br, cr[j], tr[j]);
+            tr[j] = fmaf(-bi, ci[j], tr[j]);
+            ti[j] = fmaf(br, ci[j], ti[j]);
+            ti[j] = fmaf(bi, cr[j], ti[j]);
         }
         rc_c = rc_n;
         A_c = A_n;
         rc_n = rc_nn;
         A_n = A_nn;
 
-        if ((T + 1) % tf == 0) {
-            // end of logical chunk q: its E, slots folded by one symmetric
+        if (++tc == tf) {
+            // end of logical chunk qc: its E, slots folded by one symmetric
             // add, stored per warp; state restarts for the next chunk.
             if (rcur >= 0) flush(rcur);
             rcur = -1;
-            const int q = T / tf;
 #pragma unroll
             for (int j = 0; j < NL; ++j) {
                 const float ex = er[j] + __shfl_xor_sync(0xffffffffu, er[j], 16);
                 const float ey = ei[j] + __shfl_xor_sync(0xffffffffu, ei[j], 16);
-                if (s == 0) Ew[(q * kWarps + warp) * NP + g + G * j] = make_float2(ex, ey);
+                if (s == 0) Ew[(qc * kWarps + warp) * NP + g + G * j] = make_float2(ex, ey);
                 er[j] = 0.f;
                 ei[j] = 0.f;
             }
+            tc = 0;
+            ++qc;
         }
+    };
+
+    int T = 0;
+    for (; T + 1 < total; T += 2) {
+        trip(xr, xi, nr, ni);
+        trip(nr, ni, xr, xi);
     }
+    if (T < total) trip(xr, xi, nr, ni);
     __syncthreads();
     for (int k = tid; k < nq * NP; k += kThreads) {
         const int q = k / NP, n = k - q * NP;
