@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     from concurrent.futures import ThreadPoolExecutor
 
-    objdir = os.path.join(PKG, "_lib", "obj")
+    objdir = os.path.join(ROOT, "build", "obj")
     os.makedirs(objdir, exist_ok=True)
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
 
