@@ -143,6 +143,15 @@ int hs_solve_host(hs_plan *plan, int algorithm, int iterations, int64_t subset,
                   const double *z, const double *a0, const double *theta0,
                   double *phase, double *e, double *u);
 
+/* Pipelined form of hs_solve_host: returns once the work is enqueued.  Host
+ * buffers must be page-locked (hs_host_alloc) and stay valid until hs_sync.
+ * The phase download of call k runs on a copy stream and overlaps the solve
+ * of call k+1 (device phase outputs are double-buffered). */
+int hs_solve_host_async(hs_plan *plan, int algorithm, int iterations, int64_t subset,
+                        int batch, int n, const double *x, const double *y,
+                        const double *z, const double *a0, const double *theta0,
+                        double *phase, double *e, double *u);
+
 /* Instrumentation for bench.py: the plan's cudaStream_t, the number of
  * kernels the last solve launched, and the mean device time (CUDA events,
  * `reps` back-to-back launches on the plan stream) of the kernel `which`

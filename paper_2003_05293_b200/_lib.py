@@ -42,7 +42,7 @@ EXPORTS = (
     "hs_solve_async", "hs_solve", "hs_sync", "hs_get_status", "hs_get_trace",
     "hs_get_phase", "hs_get_quality", "hs_solve_host", "hs_plan_stream",
     "hs_last_launch_count", "hs_time_kernel", "hs_fma_peak", "hs_host_alloc",
-    "hs_host_free", "hs_probe",
+    "hs_host_free", "hs_probe", "hs_solve_host_async",
 )
 
 _lib = None
@@ -80,6 +80,7 @@ def load():
             "hs_get_phase": (I, [P, I, I, P]),
             "hs_get_quality": (I, [P, P, P, P, P, P]),
             "hs_solve_host": (I, [P, I, I, I64, I, I, P, P, P, P, P, P, P, P]),
+            "hs_solve_host_async": (I, [P, I, I, I64, I, I, P, P, P, P, P, P, P, P]),
             "hs_plan_stream": (P, [P]),
             "hs_last_launch_count": (I, [P, ctypes.POINTER(I64)]),
             "hs_time_kernel": (I, [P, I, I64, I, ctypes.POINTER(D), ctypes.POINTER(D)]),

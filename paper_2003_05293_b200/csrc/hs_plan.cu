@@ -165,7 +165,11 @@ struct hs_plan {
     int32_t cnt_stride = 0;
     int32_t *d_status = nullptr, *d_degen = nullptr, *d_qstatus = nullptr;
     double *d_fields = nullptr, *d_e = nullptr, *d_u = nullptr, *d_inten = nullptr, *d_rel = nullptr;
-    double *d_phase = nullptr;   // [cap_batch][m]
+    double *d_phase = nullptr;   // [cap_batch][m] API scratch = d_out[0]
+    double *d_out[2] = {nullptr, nullptr};  // solver phase outputs (double-buffered)
+    int out_slot = 0, next_slot = 0;
+    cudaStream_t copy_stream = nullptr;     // D2H of phases, overlapped with solves
+    cudaEvent_t solved[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
     double *d_trace_w = nullptr, *d_trace_m = nullptr;
     int64_t trace_cap = 0;
 
@@ -328,7 +332,9 @@ void free_batch(hs_plan *p)
     dfree(p->d_gx); dfree(p->d_gy); dfree(p->d_w); dfree(p->d_coef);
     dfree(p->d_status); dfree(p->d_degen); dfree(p->d_qstatus);
     dfree(p->d_fields); dfree(p->d_e); dfree(p->d_u); dfree(p->d_inten); dfree(p->d_rel);
+    dfree(p->d_out[1]);
     dfree(p->d_phase);
+    p->d_out[0] = nullptr;
     dfree(p->d_trace_w); dfree(p->d_trace_m);
     free_fold(p);
     p->cap_batch = p->cap_np = 0;
@@ -351,11 +357,12 @@ int ensure_batch(hs_plan *p, int batch, int n)
         (rc = dalloc(&p->d_coef, bn)) || (rc = dalloc(&p->d_status, B)) || (rc = dalloc(&p->d_degen, B)) ||
         (rc = dalloc(&p->d_qstatus, B)) || (rc = dalloc(&p->d_fields, bn * 2)) || (rc = dalloc(&p->d_e, B)) ||
         (rc = dalloc(&p->d_u, B)) || (rc = dalloc(&p->d_inten, bn)) || (rc = dalloc(&p->d_rel, bn)) ||
-        (rc = dalloc(&p->d_phase, (size_t)B * p->m))) {
+        (rc = dalloc(&p->d_phase, (size_t)B * p->m)) || (rc = dalloc(&p->d_out[1], (size_t)B * p->m))) {
         free_batch(p);
         return rc;
     }
     CUDA_TRY(cudaMemset(p->d_status, 0, sizeof(int32_t) * B));
+    p->d_out[0] = p->d_phase;
     p->cap_batch = B;
     p->cap_np = cfg.np;
     return HS_OK;
@@ -448,7 +455,7 @@ FoldArgs fold_args(hs_plan *p, int32_t nchunks, const UpdArgs &u)
 }
 
 // Full-range fused pass with the GEMM-tile kernel (n <= 128).
-int launch_tile(hs_plan *p, bool write, const UpdArgs &u)
+int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out)
 {
     const Config &c = p->cfg;
     if (p->ntiles > p->cap_chunks) return fail(HS_ECUDA, "fold buffers too small (%d tiles)", p->ntiles);
@@ -463,7 +470,7 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u)
     a.coef = p->d_coef;
     a.amp_img = p->d_amp_img;
     a.idx_img = p->d_idx_img;
-    a.phase_out = p->d_phase;
+    a.phase_out = phase_out;
     a.phase_stride = p->m;
     a.f = fold_args(p, p->ntiles, u);
     TileFn fn = hs_select_tile(c.ns, write);
@@ -539,7 +546,7 @@ int ensure_tables(hs_plan *p)
 // update (trace record j+1, coef_{j+1}); pass j >= 1 superposes coef_j over
 // write_j (= read_{j+1}); the last pass writes the phase and yields the
 // full-range fields of quality_report.
-int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags)
+int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags, double *out)
 {
     int rc;
     const bool want_fields = (flags & HS_WANT_FIELDS) != 0;
@@ -552,9 +559,8 @@ int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags)
     const UpdArgs fin = upd_args(p, want_fields ? ACT_FINAL : ACT_NONE);
     const bool tiled = p->cfg.ns > 0;
     auto full_pass = [&](int mode, const UpdArgs &u) -> int {
-        if (tiled && (mode & PM_FWD)) return launch_tile(p, (mode & PM_WRITE) != 0, u);
-        return launch_pass(p, mode, *dense, 0, dense->count, 0, nullptr, (mode & PM_WRITE) ? p->d_phase : nullptr,
-                           m, u);
+        if (tiled && (mode & PM_FWD)) return launch_tile(p, (mode & PM_WRITE) != 0, u, out);
+        return launch_pass(p, mode, *dense, 0, dense->count, 0, nullptr, (mode & PM_WRITE) ? out : nullptr, m, u);
     };
     if (alg == HS_ALG_RS) return full_pass(final_mode, fin);
     const int cs = (subset < m) ? std::max(0, iters - 2) : 0;
@@ -592,6 +598,7 @@ int check_device(hs_plan *p)
 int sync_and_check(hs_plan *p)
 {
     CUDA_TRY(cudaStreamSynchronize(p->stream));
+    if (p->copy_stream) CUDA_TRY(cudaStreamSynchronize(p->copy_stream));
     CUDA_TRY(cudaGetLastError());
     return HS_OK;
 }
@@ -627,6 +634,11 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
     p->device = device;
     CUDA_TRY(cudaSetDevice(device));
     CUDA_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        CUDA_TRY(cudaEventCreateWithFlags(&p->solved[k], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->copied[k], cudaEventDisableTiming));
+    }
     p->side = side;
     p->m = m;
     p->c1 = prism;
@@ -704,6 +716,7 @@ void hs_plan_destroy(hs_plan *p)
     if (!p) return;
     cudaSetDevice(p->device);
     cudaStreamSynchronize(p->stream);
+    cudaStreamSynchronize(p->copy_stream);
     free_batch(p);
     free_list(p->storage);
     for (auto &kv : p->dense) free_list(kv.second);
@@ -713,6 +726,11 @@ void hs_plan_destroy(hs_plan *p)
     dfree(p->d_idx_img);
     dfree(p->d_tiles);
     cudaStreamDestroy(p->stream);
+    cudaStreamDestroy(p->copy_stream);
+    for (int k = 0; k < 2; ++k) {
+        cudaEventDestroy(p->solved[k]);
+        cudaEventDestroy(p->copied[k]);
+    }
     delete p;
 }
 
@@ -868,7 +886,14 @@ int hs_probe(hs_plan *p, const double *phase, int64_t npts, const double *xyz, i
     return sync_and_check(p);
 }
 
+static int solve_into(hs_plan *p, int alg, int iters, int64_t subset, const double *theta0, int flags, int slot);
+
 int hs_solve_async(hs_plan *p, int alg, int iters, int64_t subset, const double *theta0, int flags)
+{
+    return solve_into(p, alg, iters, subset, theta0, flags, 0);
+}
+
+static int solve_into(hs_plan *p, int alg, int iters, int64_t subset, const double *theta0, int flags, int slot)
 {
     if (p->batch < 1) return fail(HS_EINVAL, "no spots set");
     if (alg != HS_ALG_RS && alg != HS_ALG_WGS && alg != HS_ALG_CSWGS)
@@ -897,12 +922,12 @@ int hs_solve_async(hs_plan *p, int alg, int iters, int64_t subset, const double 
     }
     const size_t bytes = sizeof(double) * (size_t)p->batch * p->n;
     CUDA_TRY(cudaMemcpyAsync(p->d_theta, theta0, bytes, cudaMemcpyHostToDevice, p->stream));
-    auto key = std::make_tuple(alg, iters, subset, flags, p->batch, p->n);
+    auto key = std::make_tuple(alg, iters, subset, flags | (slot << 8), p->batch, p->n);
     auto it = p->graphs.find(key);
     if (it == p->graphs.end()) {
         cudaGraph_t graph;
         CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-        rc = record_solve(p, alg, iters, subset, flags);
+        rc = record_solve(p, alg, iters, subset, flags, p->d_out[slot]);
         cudaError_t ce = cudaStreamEndCapture(p->stream, &graph);
         if (rc) return rc;
         if (ce != cudaSuccess) return fail(HS_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce));
@@ -913,6 +938,7 @@ int hs_solve_async(hs_plan *p, int alg, int iters, int64_t subset, const double 
         it = p->graphs.emplace(key, exec).first;
     }
     CUDA_TRY(cudaGraphLaunch(it->second, p->stream));
+    p->out_slot = slot;
     p->tables_valid = true;
     p->last_alg = alg;
     p->last_iters = iters;
@@ -967,7 +993,7 @@ int hs_get_phase(hs_plan *p, int first, int count, double *phase)
     int rc;
     if ((rc = check_device(p))) return rc;
     if (count)
-        CUDA_TRY(cudaMemcpyAsync(phase, p->d_phase + (size_t)first * p->m, sizeof(double) * count * p->m,
+        CUDA_TRY(cudaMemcpyAsync(phase, p->d_out[p->out_slot] + (size_t)first * p->m, sizeof(double) * count * p->m,
                                  cudaMemcpyDeviceToHost, p->stream));
     return sync_and_check(p);
 }
@@ -989,19 +1015,38 @@ int hs_get_quality(hs_plan *p, double *e, double *u, double *intensities, double
     return sync_and_check(p);
 }
 
+// Pipelined end-to-end call: spot/theta upload, solve into phase buffer
+// `slot` (alternating), e/u download on the solve stream, and the phase
+// download on the copy stream -- it overlaps the next call's solve.  The
+// write-after-read on a phase buffer is ordered by events.
+int hs_solve_host_async(hs_plan *p, int alg, int iters, int64_t subset, int batch, int n, const double *x,
+                        const double *y, const double *z, const double *a0, const double *theta0, double *phase,
+                        double *e, double *u)
+{
+    int rc;
+    if ((rc = hs_set_spots(p, batch, n, x, y, z, a0))) return rc;
+    const int slot = p->next_slot;
+    CUDA_TRY(cudaStreamWaitEvent(p->stream, p->copied[slot], 0));
+    if ((rc = solve_into(p, alg, iters, subset, theta0, HS_WANT_FIELDS, slot))) return rc;
+    if (e) CUDA_TRY(cudaMemcpyAsync(e, p->d_e, sizeof(double) * batch, cudaMemcpyDeviceToHost, p->stream));
+    if (u) CUDA_TRY(cudaMemcpyAsync(u, p->d_u, sizeof(double) * batch, cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaEventRecord(p->solved[slot], p->stream));
+    CUDA_TRY(cudaStreamWaitEvent(p->copy_stream, p->solved[slot], 0));
+    if (phase)
+        CUDA_TRY(cudaMemcpyAsync(phase, p->d_out[slot], sizeof(double) * (size_t)batch * p->m, cudaMemcpyDeviceToHost,
+                                 p->copy_stream));
+    CUDA_TRY(cudaEventRecord(p->copied[slot], p->copy_stream));
+    p->next_slot = slot ^ 1;
+    return HS_OK;
+}
+
 int hs_solve_host(hs_plan *p, int alg, int iters, int64_t subset, int batch, int n, const double *x,
                   const double *y, const double *z, const double *a0, const double *theta0, double *phase,
                   double *e, double *u)
 {
-    int rc;
-    if ((rc = hs_set_spots(p, batch, n, x, y, z, a0))) return rc;
-    if ((rc = hs_solve_async(p, alg, iters, subset, theta0, HS_WANT_FIELDS))) return rc;
-    if (phase)
-        CUDA_TRY(cudaMemcpyAsync(phase, p->d_phase, sizeof(double) * (size_t)batch * p->m, cudaMemcpyDeviceToHost,
-                                 p->stream));
-    if (e) CUDA_TRY(cudaMemcpyAsync(e, p->d_e, sizeof(double) * batch, cudaMemcpyDeviceToHost, p->stream));
-    if (u) CUDA_TRY(cudaMemcpyAsync(u, p->d_u, sizeof(double) * batch, cudaMemcpyDeviceToHost, p->stream));
-    return sync_and_check(p);
+    int rc = hs_solve_host_async(p, alg, iters, subset, batch, n, x, y, z, a0, theta0, phase, e, u);
+    if (rc) return rc;
+    return hs_sync(p);
 }
 
 void *hs_plan_stream(hs_plan *p) { return (void *)p->stream; }
@@ -1034,7 +1079,7 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
     CUDA_TRY(cudaEventCreate(&e1));
     const UpdArgs u = upd_args(p, ACT_FIELDS);
     auto once = [&]() -> int {
-        if (which == 0 && p->cfg.ns > 0) return launch_tile(p, false, u);
+        if (which == 0 && p->cfg.ns > 0) return launch_tile(p, false, u, nullptr);
         return launch_pass(p, PM_BWD | PM_FWD, *l, 0, l->count, 0, nullptr, nullptr, 0, u);
     };
     if ((rc = reset_status(p)) || (rc = once())) return rc;

@@ -261,3 +261,46 @@ def test_large_spot_count_path(pupils, rng):
     mags = np.array([rec.magnitudes for rec in trace.records])
     assert np.all(np.abs(mags - r["mags"]) <= 1e-4 * r["mags"])
     masked_phase_check(p, s, holo.phase, r["amps"], r["thetas"], tab=r["tables"])
+
+
+def test_pipelined_host_api_matches_batch(pupils):
+    """hs_solve_host_async: back-to-back calls with double-buffered outputs
+    return the same phases / e / u as solve_batch."""
+    import ctypes
+    import math
+    from paper_2003_05293_b200 import _lib
+    p = pupils["p512g0"]
+    lib = _lib.load()
+    plan = _lib.Plan(p)
+    cfg = hs.SolverConfig("cswgs", iterations=6, compression=1 / 8, seed=0)
+    sub = math.ceil(p.active_count / 8)
+    calls, keep = [], []
+
+    def pinned(arr):
+        ptr = lib.hs_host_alloc(arr.nbytes)
+        view = np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_double)),
+                                     shape=arr.shape)
+        view[...] = arr
+        keep.append(ptr)
+        return ptr, view
+
+    for k in range(3):
+        sets = [hs.random_foci(10, 50 + 2 * k + b) for b in range(2)]
+        th = np.stack([np.random.default_rng(10 * k + b).random(10) * 2 * math.pi
+                       for b in range(2)])
+        bufs = [pinned(np.stack([getattr(s, f) for s in sets])) for f in ("x", "y", "z", "amplitude")]
+        thb = pinned(th)
+        ph = pinned(np.zeros((2, p.active_count)))
+        e = pinned(np.zeros(2))
+        u = pinned(np.zeros(2))
+        _lib.check(lib.hs_solve_host_async(plan.handle, _lib.ALG_CSWGS, 6, sub, 2, 10,
+                                           *[b[0] for b in bufs], thb[0], ph[0], e[0], u[0]))
+        calls.append((sets, [10 * k, 10 * k + 1], ph[1], e[1], u[1]))
+    plan.sync()
+    for sets, seeds, ph, e, u in calls:
+        want = hs.solve_batch(p, sets, cfg, seeds=seeds)
+        for b in range(2):
+            assert np.array_equal(ph[b], want[b][0].phase)
+            assert e[b] == want[b][1].quality.efficiency and u[b] == want[b][1].quality.uniformity
+    for ptr in keep:
+        lib.hs_host_free(ptr)
