@@ -152,6 +152,27 @@ int hs_solve_host_async(hs_plan *plan, int algorithm, int iterations, int64_t su
                         const double *z, const double *a0, const double *theta0,
                         double *phase, double *e, double *u);
 
+/* Row-sharded solve of one batch across `world` processes (one per GPU,
+ * SURVEY.md 8(e)).  Every rank calls, with identical spots and theta0:
+ *   hs_shard_begin(...);
+ *   for j in 0 .. passes-1   (passes = 1 for RS, iterations + 1 otherwise):
+ *       hs_shard_pass(j, local, &g_lo, &g_hi, &ngroups);
+ *       all_groups = all-gather(local) in rank order   (caller: NCCL / gloo)
+ *       hs_shard_update(j, all_groups, ngroups);
+ * `local` / `all_groups` hold complex128 group partials laid out
+ * [batch][groups][np] (np = hs_padded_spots).  Ranks own fold-group-aligned
+ * chunk ranges (pixel-row slabs), so every rank folds the same group
+ * sequence: fields, weights, e/u are bitwise identical on all ranks and to
+ * hs_solve.  Phases of pixels another rank owns are NaN in hs_get_phase. */
+int hs_shard_begin(hs_plan *plan, int algorithm, int iterations, int64_t subset,
+                   const double *theta0, int rank, int world);
+int hs_shard_pass(hs_plan *plan, int pass, double *local_groups, int *g_lo, int *g_hi,
+                  int *ngroups);
+int hs_shard_update(hs_plan *plan, int pass, const double *all_groups, int ngroups);
+/* Group range [g_lo, g_hi) of this rank and the total group count of pass j. */
+int hs_shard_groups(hs_plan *plan, int pass, int *g_lo, int *g_hi, int *ngroups);
+int hs_padded_spots(hs_plan *plan);
+
 /* Instrumentation for bench.py: the plan's cudaStream_t, the number of
  * kernels the last solve launched, and the mean device time (CUDA events,
  * `reps` back-to-back launches on the plan stream) of the kernel `which`

@@ -42,7 +42,8 @@ EXPORTS = (
     "hs_solve_async", "hs_solve", "hs_sync", "hs_get_status", "hs_get_trace",
     "hs_get_phase", "hs_get_quality", "hs_solve_host", "hs_plan_stream",
     "hs_last_launch_count", "hs_time_kernel", "hs_fma_peak", "hs_host_alloc",
-    "hs_host_free", "hs_probe", "hs_solve_host_async",
+    "hs_host_free", "hs_probe", "hs_solve_host_async", "hs_shard_begin", "hs_shard_pass",
+    "hs_shard_update", "hs_padded_spots", "hs_shard_groups",
 )
 
 _lib = None
@@ -85,6 +86,11 @@ def load():
             "hs_last_launch_count": (I, [P, ctypes.POINTER(I64)]),
             "hs_time_kernel": (I, [P, I, I64, I, ctypes.POINTER(D), ctypes.POINTER(D)]),
             "hs_fma_peak": (I, [I, ctypes.POINTER(D)]),
+            "hs_shard_begin": (I, [P, I, I, I64, P, I, I]),
+            "hs_shard_pass": (I, [P, I, P, ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(I)]),
+            "hs_shard_update": (I, [P, I, P, I]),
+            "hs_shard_groups": (I, [P, I, ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(I)]),
+            "hs_padded_spots": (I, [P]),
             "hs_probe": (I, [P, P, I64, P, I, P]),
             "hs_host_alloc": (P, [I64]),
             "hs_host_free": (None, [P]),
@@ -249,6 +255,32 @@ class Plan:
         finally:
             self._spots_key = None  # hs_probe replaced the device spot set
         return out
+
+    # ---- row-sharded solve (distributed.solve_sharded) -----------------
+    def shard_begin(self, algorithm: int, iterations: int, subset: int, theta0, rank: int,
+                    world: int) -> None:
+        check(load().hs_shard_begin(self.handle, algorithm, iterations, subset,
+                                    ptr(f64(theta0)), rank, world))
+
+    def shard_pass(self, j: int):
+        """Run pass j on this rank's chunk range -> (group partials
+        complex128 [B][g_hi - g_lo][np], g_lo, g_hi, total groups)."""
+        lib = load()
+        np_ = lib.hs_padded_spots(self.handle)
+        lo, hi, ng = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        check(lib.hs_shard_groups(self.handle, j, ctypes.byref(lo), ctypes.byref(hi),
+                                  ctypes.byref(ng)))
+        local = np.zeros((self.batch, hi.value - lo.value, np_), dtype=np.complex128)
+        check(lib.hs_shard_pass(self.handle, j, ptr(local), ctypes.byref(lo), ctypes.byref(hi),
+                                ctypes.byref(ng)))
+        return local, lo.value, hi.value, ng.value
+
+    def shard_update(self, j: int, all_groups: np.ndarray) -> None:
+        g = np.ascontiguousarray(all_groups, dtype=np.complex128)
+        check(load().hs_shard_update(self.handle, j, ptr(g), g.shape[1]))
+
+    def padded_spots(self) -> int:
+        return int(load().hs_padded_spots(self.handle))
 
     def stream(self) -> int:
         return int(load().hs_plan_stream(self.handle) or 0)

@@ -64,6 +64,8 @@ struct UpdArgs {
 // Cross-CTA fold state shared by the pass and tile kernels.
 struct FoldArgs {
     int32_t nchunks;          // partials per pattern in this launch
+    int32_t chunk_base;       // first chunk of this launch (row-sharded passes)
+    int32_t chunk_end;        // one past the last chunk of this launch
     int32_t np;
     float2 *partials;         // [B][part_stride]: [chunk][np]
     int64_t part_stride;
@@ -363,7 +365,7 @@ hs_pass_kernel(const PassArgs a)
     extern __shared__ float4 smem4[];
 
     const int pat = blockIdx.y;
-    const int chunk = blockIdx.x;
+    const int chunk = a.f.chunk_base + blockIdx.x;
     if (a.f.u.status[pat] != 0) return;  // pattern already failed (uniform per CTA)
 
     const int tid = threadIdx.x;
@@ -581,5 +583,48 @@ PassFn hs_select_g32(int nl, int mode);
         default: return nullptr;                              \
         }                                                     \
     }
+
+// ---------------------------------------------------------------------------
+// Row-sharded passes (paper_2003_05293_b200/distributed.py): the chunk range of
+// a rank is folded group by group (same order and precision as hs_fold's first
+// level), the group partials of all ranks are exchanged, and every rank runs
+// the second level + update on the identical group sequence.
+static __global__ void hs_group_fold_kernel(FoldArgs a, int g_lo)
+{
+    const int pat = blockIdx.y, grp = g_lo + blockIdx.x, np = a.np;
+    const int c0 = grp * kGroup, c1 = min(c0 + kGroup, a.nchunks);
+    const float2 *part = a.partials + (int64_t)pat * a.part_stride;
+    double2 *gp = a.gpart + (int64_t)pat * a.gpart_stride;
+    for (int k = threadIdx.x; k < np; k += blockDim.x) {
+        double sx = 0.0, sy = 0.0;
+        for (int c = c0; c < c1; ++c) {
+            const float2 v = part[(int64_t)c * np + k];
+            sx += (double)v.x;
+            sy += (double)v.y;
+        }
+        gp[(int64_t)grp * np + k] = make_double2(sx, sy);
+    }
+}
+
+static __global__ void __launch_bounds__(kThreads) hs_fold_update_kernel(FoldArgs a, int ngroups)
+{
+    __shared__ double dbuf[kThreads];
+    __shared__ int ibuf[kThreads];
+    extern __shared__ double2 Eu[];          // [np] fields + [2 np] scratch
+    const int pat = blockIdx.x, np = a.np;
+    if (a.u.status[pat] != 0) return;
+    const double2 *gp = a.gpart + (int64_t)pat * a.gpart_stride;
+    for (int k = threadIdx.x; k < np; k += kThreads) {
+        double sx = 0.0, sy = 0.0;
+        for (int g = 0; g < ngroups; ++g) {
+            const double2 v = gp[(int64_t)g * np + k];
+            sx += v.x;
+            sy += v.y;
+        }
+        Eu[k] = make_double2(sx, sy);
+    }
+    __syncthreads();
+    hs_update(a.u, pat, Eu, reinterpret_cast<double *>(Eu + np), dbuf, ibuf);
+}
 
 }  // namespace hs

@@ -174,6 +174,12 @@ struct hs_plan {
     int64_t trace_cap = 0;
 
     int last_alg = -1, last_iters = 0, last_flags = 0;
+    // row-sharded solve state (hs_shard_*)
+    struct {
+        bool active = false;
+        int rank = 0, world = 1, alg = 0, iters = 0, cs = 0, passes = 0;
+        int64_t subset = 0, half = 1;
+    } shard;
     int64_t last_launches = 0;
     std::map<std::tuple<int, int, int64_t, int, int, int>, cudaGraphExec_t> graphs;
 };
@@ -438,10 +444,12 @@ int launch_tables(hs_plan *p, bool seed)
     return HS_OK;
 }
 
-FoldArgs fold_args(hs_plan *p, int32_t nchunks, const UpdArgs &u)
+FoldArgs fold_args(hs_plan *p, int32_t nchunks, const UpdArgs &u, int32_t lo = 0, int32_t hi = -1)
 {
     FoldArgs f;
     f.nchunks = nchunks;
+    f.chunk_base = lo;
+    f.chunk_end = hi < 0 ? nchunks : hi;
     f.np = p->cfg.np;
     f.partials = p->d_part;
     f.part_stride = p->part_stride;
@@ -455,8 +463,9 @@ FoldArgs fold_args(hs_plan *p, int32_t nchunks, const UpdArgs &u)
 }
 
 // Full-range fused pass with the GEMM-tile kernel (n <= 128).
-int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out)
+int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int32_t lo = 0, int32_t hi = -1)
 {
+    if (hi < 0) hi = p->ntiles;
     const Config &c = p->cfg;
     if (p->ntiles > p->cap_chunks) return fail(HS_ECUDA, "fold buffers too small (%d tiles)", p->ntiles);
     TileArgs a;
@@ -472,9 +481,10 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out)
     a.idx_img = p->d_idx_img;
     a.phase_out = phase_out;
     a.phase_stride = p->m;
-    a.f = fold_args(p, p->ntiles, u);
+    a.f = fold_args(p, p->ntiles, u, lo, hi);
     TileFn fn = hs_select_tile(c.ns, write);
-    dim3 grid(p->ntiles, p->batch);
+    if (hi <= lo) return HS_OK;
+    dim3 grid(hi - lo, p->batch);
     fn<<<grid, kThreads, hs_tile_smem_bytes(c.ns), p->stream>>>(a);
     CUDA_TRY(cudaGetLastError());
     return HS_OK;
@@ -482,7 +492,8 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out)
 
 // One pass over `count` entries of list `l` starting at entry `off`.
 int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t count, int64_t idx_base,
-                const double *phase_in, double *phase_out, int64_t phase_stride, const UpdArgs &u)
+                const double *phase_in, double *phase_out, int64_t phase_stride, const UpdArgs &u,
+                int32_t lo = 0, int32_t hi = -1)
 {
     const Config &c = p->cfg;
     const Geom geo = geom_of(l, count, c.spw);
@@ -506,15 +517,17 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
     a.phase_in = phase_in;
     a.phase_out = phase_out;
     a.phase_stride = phase_stride;
-    a.f = fold_args(p, geo.nchunks, u);
-    dim3 grid(geo.nchunks, p->batch);
+    if (hi < 0) hi = geo.nchunks;
+    if (hi <= lo) return HS_OK;
+    a.f = fold_args(p, geo.nchunks, u, lo, hi);
+    dim3 grid(hi - lo, p->batch);
     if (l.sorted_rows && c.ns > 0 && mode == (PM_BWD | PM_FWD)) {
         // compressed window: latency-shaped kernel (16 lanes per pixel); a
         // CTA streams cpc logical chunks when the batch gives enough CTAs
         int cpc = 1;
         while (cpc < kMaxCpc && (int64_t)geo.nchunks * p->batch / (2 * cpc) >= 4 * kTargetChunks) cpc *= 2;
         a.cpc = cpc;
-        grid.x = (geo.nchunks + cpc - 1) / cpc;
+        grid.x = (hi - lo + cpc - 1) / cpc;
         hs_select_win(c.ns, p->win_minb)<<<grid, kThreads, hs_win_smem_bytes(c.ns), p->stream>>>(a);
     } else {
         PassFn fn = select_pass(c, mode);
@@ -622,6 +635,8 @@ int hs_device_count(int *count)
 }
 
 int hs_max_spots(void) { return 1024; }
+
+int hs_padded_spots(hs_plan *p) { return p->cfg.np; }
 
 int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const int64_t *cols,
                    const double *amplitude, const double *axis, double prism, double lens,
@@ -1047,6 +1062,154 @@ int hs_solve_host(hs_plan *p, int alg, int iters, int64_t subset, int batch, int
     int rc = hs_solve_host_async(p, alg, iters, subset, batch, n, x, y, z, a0, theta0, phase, e, u);
     if (rc) return rc;
     return hs_sync(p);
+}
+
+// ------------------------------------------------------------------
+// Row-sharded solve (one process per GPU).  Pass j of the schedule runs over
+// the rank's fold-group-aligned chunk range; hs_shard_pass returns the
+// rank's group partials, the caller all-gathers them (rank order = group
+// order) and hs_shard_update folds all groups in order and applies the
+// update -- identical on every rank and bitwise equal to hs_solve.
+static void shard_range(int nchunks, int rank, int world, int *lo, int *hi)
+{
+    const int ng = (nchunks + kGroup - 1) / kGroup;
+    const int g0 = (int)((int64_t)rank * ng / world), g1 = (int)((int64_t)(rank + 1) * ng / world);
+    *lo = std::min(g0 * kGroup, nchunks);
+    *hi = std::min(g1 * kGroup, nchunks);
+}
+
+// pass j: kind 0 = tile pass, 1 = list pass; list + chunk count
+static int shard_pass_desc(hs_plan *p, int j, int *kind, const DevList **list, int *nchunks)
+{
+    auto &sh = p->shard;
+    const int64_t m = p->m;
+    const DevList *lst = nullptr;
+    int rc;
+    if (sh.alg != HS_ALG_RS && (j == 0 ? sh.cs > 0 : j <= sh.cs)) {
+        const int64_t off = (j == 0) ? 0 : ((int64_t)(j - 1) * sh.half) % (m - sh.subset + 1);
+        if ((rc = get_window(p, off, sh.subset, &lst))) return rc;
+        *kind = 1;
+    } else if (p->cfg.ns > 0) {
+        *kind = 0;
+        *list = nullptr;
+        *nchunks = p->ntiles;
+        return HS_OK;
+    } else {
+        if ((rc = get_dense(p, p->cfg.spw, &lst))) return rc;
+        *kind = 1;
+    }
+    *list = lst;
+    *nchunks = geom_of(*lst, lst->count, p->cfg.spw).nchunks;
+    return HS_OK;
+}
+
+int hs_shard_begin(hs_plan *p, int alg, int iters, int64_t subset, const double *theta0, int rank, int world)
+{
+    if (p->batch < 1) return fail(HS_EINVAL, "no spots set");
+    if (world < 1 || rank < 0 || rank >= world) return fail(HS_EINVAL, "invalid rank %d / world %d", rank, world);
+    if (alg != HS_ALG_RS && alg != HS_ALG_WGS && alg != HS_ALG_CSWGS) return fail(HS_EINVAL, "unknown algorithm");
+    if (alg == HS_ALG_RS) {
+        iters = 0;
+        subset = p->m;
+    } else {
+        if (iters < 1) return fail(HS_EINVAL, "iterations must be >= 1");
+        if (alg == HS_ALG_CSWGS && iters < 2) return fail(HS_EINVAL, "cswgs needs iterations >= 2");
+        if (alg == HS_ALG_WGS) subset = p->m;
+        if (subset < 1 || subset > p->m) return fail(HS_EINVAL, "subset size outside 1..M");
+    }
+    if (!(p->sum_amp > 0.0)) return fail(HS_EZEROILLUM, "pupil carries no illumination");
+    int rc;
+    if ((rc = check_device(p)) || (rc = ensure_trace(p, iters))) return rc;
+    auto &sh = p->shard;
+    sh.active = true;
+    sh.rank = rank;
+    sh.world = world;
+    sh.alg = alg;
+    sh.iters = iters;
+    sh.subset = subset;
+    sh.cs = (alg != HS_ALG_RS && subset < p->m) ? std::max(0, iters - 2) : 0;
+    sh.half = std::max<int64_t>(1, subset / 2);
+    sh.passes = (alg == HS_ALG_RS) ? 1 : iters + 1;
+    const size_t bytes = sizeof(double) * (size_t)p->batch * p->n;
+    CUDA_TRY(cudaMemcpyAsync(p->d_theta, theta0, bytes, cudaMemcpyHostToDevice, p->stream));
+    if ((rc = reset_status(p)) || (rc = launch_tables(p, true))) return rc;
+    // phases this rank does not own stay NaN (0xff bytes) for the merge
+    CUDA_TRY(cudaMemsetAsync(p->d_out[0], 0xff, sizeof(double) * (size_t)p->batch * p->m, p->stream));
+    p->tables_valid = true;
+    p->out_slot = 0;
+    p->last_alg = alg;
+    p->last_iters = iters;
+    p->last_flags = HS_WANT_FIELDS;
+    return HS_OK;
+}
+
+int hs_shard_pass(hs_plan *p, int j, double *groups, int *g_lo, int *g_hi, int *ngroups)
+{
+    auto &sh = p->shard;
+    if (!sh.active || j < 0 || j >= sh.passes) return fail(HS_EINVAL, "shard pass %d out of range", j);
+    int rc, kind, nch;
+    const DevList *lst;
+    if ((rc = check_device(p)) || (rc = shard_pass_desc(p, j, &kind, &lst, &nch))) return rc;
+    int lo, hi;
+    shard_range(nch, sh.rank, sh.world, &lo, &hi);
+    const bool last = (j == sh.passes - 1);
+    const int mode = last ? (PM_BWD | PM_FWD | PM_WRITE) : (PM_BWD | PM_FWD);
+    const UpdArgs none = upd_args(p, ACT_NONE);
+    if (kind == 0)
+        rc = launch_tile(p, last, none, p->d_out[0], lo, hi);
+    else
+        rc = launch_pass(p, mode, *lst, 0, lst->count, 0, nullptr, last ? p->d_out[0] : nullptr, p->m, none, lo, hi);
+    if (rc) return rc;
+    const int ng = (nch + kGroup - 1) / kGroup;
+    *g_lo = lo / kGroup;
+    *g_hi = (hi + kGroup - 1) / kGroup;
+    *ngroups = ng;
+    if (*g_hi > *g_lo) {
+        hs_group_fold_kernel<<<dim3(*g_hi - *g_lo, p->batch), 128, 0, p->stream>>>(fold_args(p, nch, none, lo, hi),
+                                                                                *g_lo);
+        CUDA_TRY(cudaGetLastError());
+        const int np = p->cfg.np, cnt = *g_hi - *g_lo;
+        if (groups)
+            CUDA_TRY(cudaMemcpy2DAsync(groups, sizeof(double2) * cnt * np,
+                                       p->d_gpart + (int64_t)*g_lo * np, sizeof(double2) * p->gpart_stride,
+                                       sizeof(double2) * cnt * np, p->batch, cudaMemcpyDeviceToHost, p->stream));
+    }
+    return sync_and_check(p);
+}
+
+int hs_shard_groups(hs_plan *p, int j, int *g_lo, int *g_hi, int *ngroups)
+{
+    auto &sh = p->shard;
+    if (!sh.active || j < 0 || j >= sh.passes) return fail(HS_EINVAL, "shard pass %d out of range", j);
+    int rc, kind, nch, lo, hi;
+    const DevList *lst;
+    if ((rc = shard_pass_desc(p, j, &kind, &lst, &nch))) return rc;
+    shard_range(nch, sh.rank, sh.world, &lo, &hi);
+    *g_lo = lo / kGroup;
+    *g_hi = (hi + kGroup - 1) / kGroup;
+    *ngroups = (nch + kGroup - 1) / kGroup;
+    return HS_OK;
+}
+
+int hs_shard_update(hs_plan *p, int j, const double *groups, int ngroups)
+{
+    auto &sh = p->shard;
+    if (!sh.active || j < 0 || j >= sh.passes) return fail(HS_EINVAL, "shard pass %d out of range", j);
+    int rc;
+    if ((rc = check_device(p))) return rc;
+    const int np = p->cfg.np;
+    if ((int64_t)ngroups * np > p->gpart_stride) return fail(HS_EINVAL, "too many groups");
+    CUDA_TRY(cudaMemcpy2DAsync(p->d_gpart, sizeof(double2) * p->gpart_stride, groups,
+                               sizeof(double2) * ngroups * np, sizeof(double2) * ngroups * np, p->batch,
+                               cudaMemcpyHostToDevice, p->stream));
+    const bool last = (j == sh.passes - 1);
+    UpdArgs u = upd_args(p, last ? ACT_FINAL : ACT_STEP);
+    u.iter = j;
+    u.iters = std::max(sh.iters, 1);
+    hs_fold_update_kernel<<<p->batch, kThreads, sizeof(double2) * 2 * np, p->stream>>>(fold_args(p, 0, u), ngroups);
+    CUDA_TRY(cudaGetLastError());
+    if (last) sh.active = false;
+    return sync_and_check(p);
 }
 
 void *hs_plan_stream(hs_plan *p) { return (void *)p->stream; }

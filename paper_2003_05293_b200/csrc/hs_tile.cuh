@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tile_kernel(const TileArgs a)
     float2 *Rs = Vs + kTileC * kBS;       // [16][NP]        (after forward)
 
     const int pat = blockIdx.y;
-    const int tile = blockIdx.x;
+    const int tile = a.f.chunk_base + blockIdx.x;
     if (a.f.u.status[pat] != 0) return;
     const int tid = threadIdx.x;
     const int packed = __ldg(a.tiles + tile);

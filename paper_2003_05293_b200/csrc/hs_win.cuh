@@ -44,8 +44,8 @@ __global__ void __launch_bounds__(kThreads, MINB) hs_win_kernel(const PassArgs a
 
     const int pat = blockIdx.y;
     if (a.f.u.status[pat] != 0) return;
-    const int q0 = blockIdx.x * a.cpc;
-    const int nq = min(a.cpc, a.f.nchunks - q0);
+    const int q0 = a.f.chunk_base + blockIdx.x * a.cpc;
+    const int nq = min(a.cpc, a.f.chunk_end - q0);
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int g = lane & (G - 1), s = lane / G;

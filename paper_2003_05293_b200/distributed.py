@@ -79,3 +79,68 @@ def sharded_fields(partials: np.ndarray, world: int, rank: int, all_gather) -> n
     local = fold_groups(partials, lo, hi)
     gathered = all_gather(local)
     return fold_fields(np.concatenate([g for g in gathered if g.size], axis=0))
+
+
+# ---------------------------------------------------------------- device path
+def solve_sharded(pupil, spots, config, rank: int, world: int, all_gather, device=None):
+    """Row-sharded solve of one pattern across ``world`` processes.
+
+    Every rank calls this with the same ``spots`` / ``config``;
+    ``all_gather(obj) -> list`` (rank order) exchanges the per-pass group
+    partials (``ngroups x np`` complex128 per pass) and finally the phase
+    slabs.  Returns ``(Hologram, SolverTrace)`` identical on every rank and
+    bitwise equal to :func:`paper_2003_05293_b200.solve` on one GPU.
+    """
+    import time
+
+    from . import _lib
+    from .optics import CompressionPlan, Hologram
+    from .solvers import (SolverConfig, SolverTrace, StepRecord, _ALG_CODE, _raise_status,
+                          _theta0, window_sizes)
+
+    if not isinstance(config, SolverConfig):
+        raise TypeError("config must be a SolverConfig")
+    t0 = time.perf_counter()
+    m, n = pupil.active_count, spots.count
+    subset = m
+    if config.algorithm == "cswgs":
+        subset = CompressionPlan.for_pupil(pupil, config.compression).subset_size
+    iters = 0 if config.algorithm == "rs" else config.iterations
+    plan = _lib.plan_for(pupil, device)
+    plan.set_spots(spots)
+    plan.shard_begin(_ALG_CODE[config.algorithm], iters, subset, _theta0(config.seed, n),
+                     rank, world)
+    passes = 1 if config.algorithm == "rs" else iters + 1
+    for j in range(passes):
+        local, g_lo, g_hi, ngroups = plan.shard_pass(j)
+        pieces = all_gather((g_lo, g_hi, local))
+        order = sorted(pieces, key=lambda t: t[0])
+        groups = np.concatenate([t[2] for t in order if t[2].shape[1]], axis=1)
+        if groups.shape[1] != ngroups:
+            raise RuntimeError(f"group exchange incomplete: {groups.shape[1]} of {ngroups}")
+        plan.shard_update(j, groups)
+    status, deg = plan.status()
+    _raise_status(int(status[0]))
+    mine = plan.phases()[0]
+    slabs = all_gather(mine)
+    phase = np.full(m, np.nan)
+    for sl in slabs:
+        own = ~np.isnan(sl)
+        phase[own] = sl[own]
+    if np.isnan(phase).any():
+        raise RuntimeError("phase slabs do not cover the pupil")
+    holo = Hologram(phase, pupil)
+    e, u, inten, rel, _ = plan.quality_batch()
+    from .metrics import QualityReport
+    fused = QualityReport(float(e[0]), float(u[0]), inten[0].copy(), rel[0].copy())
+    if config.algorithm == "rs":
+        return holo, SolverTrace("rs", (), m * n, time.perf_counter() - t0, False, holo, fused)
+    w, mg = plan.trace(iters)
+    records, ops = [], 0
+    first = int(deg[0])
+    for j, size in enumerate(window_sizes(m, subset, iters), start=1):
+        ops += size * n
+        records.append(StepRecord(j, w[0, j - 1].copy(), mg[0, j - 1].copy(), size, ops,
+                                  bool(first and j >= first)))
+    return holo, SolverTrace(config.algorithm, tuple(records), ops, time.perf_counter() - t0,
+                             bool(first), holo, fused)
