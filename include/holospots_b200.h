@@ -57,6 +57,7 @@ extern "C" {
 
 /* hs_solve flags */
 #define HS_WANT_FIELDS 1   /* fuse the full-range e/u projection into the last pass */
+#define HS_WANT_RASTER 2   /* also write the SLM gray raster (default linear LUT) */
 
 typedef struct hs_plan hs_plan;
 
@@ -108,6 +109,16 @@ int hs_quality(hs_plan *plan, const double *phase, double *e, double *u,
  * bit).  Replaces the plan's current spot set. */
 int hs_probe(hs_plan *plan, const double *phase, int64_t npts, const double *xyz,
              int batch, double *out);
+
+/* SLM gray raster [side][side] (uint8, 0 outside the aperture) of a
+ * storage-order phase[m] through a 256-entry phase LUT (NULL = the default
+ * linear table); equals write_hologram_pgm's raster (fileio.py:233-241,
+ * PhaseLut.gray fileio.py:202-213) bit for bit. */
+int hs_raster(hs_plan *plan, const double *phase, const double *lut, unsigned char *out);
+
+/* Rasters [count][side][side] built by the last pass of a solve run with
+ * HS_WANT_RASTER (linear LUT fused into the phase write). */
+int hs_get_raster(hs_plan *plan, int first, int count, unsigned char *out);
 
 /* Run `algorithm` on all patterns of the current spot batch.
  * iterations: I (ignored for RS); subset: ceil(c*M) for CS-WGS (M for WGS);

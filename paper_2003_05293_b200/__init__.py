@@ -21,6 +21,7 @@ from .solvers import (PlannedRun, SolverConfig, SolverTrace, StepRecord, WgsStat
                       budget_controller, cswgs, predict_ops, rebalance_weights, rs, solve,
                       solve_batch, wgs, wgs_step)
 from .simulate import FieldImage, probe_intensities, render_plane
+from .slm import PhaseLut, slm_raster, solve_rasters
 from ._lib import get_device, set_device
 from .workloads import grid_spots, named_spots, random_foci
 

@@ -24,6 +24,7 @@ HS_OK, HS_EINVAL, HS_EGEOMETRY, HS_EDEGENERATE, HS_EDIVERGED, HS_ECUDA, \
     HS_EZEROILLUM, HS_EUNDEFINED = range(8)
 ALG_RS, ALG_WGS, ALG_CSWGS = 0, 1, 2
 WANT_FIELDS = 1
+WANT_RASTER = 2
 
 _ERRORS = {
     HS_EINVAL: InvalidParameterError,
@@ -43,7 +44,7 @@ EXPORTS = (
     "hs_get_phase", "hs_get_quality", "hs_solve_host", "hs_plan_stream",
     "hs_last_launch_count", "hs_time_kernel", "hs_fma_peak", "hs_host_alloc",
     "hs_host_free", "hs_probe", "hs_solve_host_async", "hs_shard_begin", "hs_shard_pass",
-    "hs_shard_update", "hs_padded_spots", "hs_shard_groups",
+    "hs_shard_update", "hs_padded_spots", "hs_shard_groups", "hs_raster", "hs_get_raster",
 )
 
 _lib = None
@@ -89,6 +90,8 @@ def load():
             "hs_shard_begin": (I, [P, I, I, I64, P, I, I]),
             "hs_shard_pass": (I, [P, I, P, ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(I)]),
             "hs_shard_update": (I, [P, I, P, I]),
+            "hs_raster": (I, [P, P, P, P]),
+            "hs_get_raster": (I, [P, I, I, P]),
             "hs_shard_groups": (I, [P, I, ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(I)]),
             "hs_padded_spots": (I, [P]),
             "hs_probe": (I, [P, P, I64, P, I, P]),
@@ -210,11 +213,23 @@ class Plan:
 
     # ---- solver ---------------------------------------------------------
     def solve(self, algorithm: int, iterations: int, subset: int, theta0,
-              want_fields: bool = True, sync: bool = True) -> None:
+              want_fields: bool = True, sync: bool = True, raster: bool = False) -> None:
         th = f64(theta0)
         fn = load().hs_solve if sync else load().hs_solve_async
-        check(fn(self.handle, algorithm, iterations, subset, ptr(th),
-                 WANT_FIELDS if want_fields else 0))
+        flags = (WANT_FIELDS if want_fields else 0) | (WANT_RASTER if raster else 0)
+        check(fn(self.handle, algorithm, iterations, subset, ptr(th), flags))
+
+    def rasters(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        count = self.batch - first if count is None else count
+        out = np.empty((count, self.side, self.side), dtype=np.uint8)
+        check(load().hs_get_raster(self.handle, first, count, ptr(out)))
+        return out
+
+    def raster(self, phase, lut=None) -> np.ndarray:
+        out = np.empty((self.side, self.side), dtype=np.uint8)
+        tab = None if lut is None else f64(lut)
+        check(load().hs_raster(self.handle, ptr(f64(phase)), ptr(tab), ptr(out)))
+        return out
 
     def sync(self) -> None:
         check(load().hs_sync(self.handle))

@@ -92,6 +92,8 @@ struct PassArgs {
     const float2 *coef;       // [B][np]
     const double *phase_in;   // [B][phase_stride] (PM_FWD without PM_BWD)
     double *phase_out;        // [B][phase_stride] (PM_WRITE)
+    unsigned char *raster;    // [B][side][side] SLM gray raster (PM_WRITE, nullable)
+    int32_t side;
     int64_t phase_stride;
     FoldArgs f;
 };
@@ -104,6 +106,16 @@ __device__ __forceinline__ double hs_wrap(double t)
     if (w >= kPi) w -= kTwoPi;
     if (w < -kPi) w += kTwoPi;
     return w;
+}
+
+// Linear phase -> gray lookup of the default PhaseLut (fileio.py:159-213):
+// g = rint((p + pi) * 256 / (2 pi)) mod 256 on the wrapped fp64 phase, with
+// the reference's operation order (no contraction), so a device raster equals
+// PhaseLut.default().gray(phase) bit for bit.
+__device__ __forceinline__ unsigned char hs_gray_linear(double p)
+{
+    const double g = rint(__dmul_rn(__dadd_rn(p, kPi), 256.0 / kTwoPi));
+    return (unsigned char)(((long long)g) & 255);
 }
 
 __device__ __forceinline__ void hs_seed_one(int b, int k, int n, int np, const double *amp,
@@ -505,6 +517,9 @@ hs_pass_kernel(const PassArgs a)
                         else if (ph < -kPi) ph += kTwoPi;  // fp32 -pi lies below fp64 -pi
                     }
                     a.phase_out[(int64_t)pat * a.phase_stride + di] = ph;
+                    if (a.raster)
+                        a.raster[(int64_t)pat * a.side * a.side + (int64_t)(rc >> 16) * a.side + (rc & 0xffff)] =
+                            hs_gray_linear(ph);
                 }
             }
         } else {

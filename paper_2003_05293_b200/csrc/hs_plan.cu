@@ -167,6 +167,7 @@ struct hs_plan {
     double *d_fields = nullptr, *d_e = nullptr, *d_u = nullptr, *d_inten = nullptr, *d_rel = nullptr;
     double *d_phase = nullptr;   // [cap_batch][m] API scratch = d_out[0]
     double *d_out[2] = {nullptr, nullptr};  // solver phase outputs (double-buffered)
+    unsigned char *d_raster = nullptr;      // [cap_batch][side][side] SLM gray rasters
     int out_slot = 0, next_slot = 0;
     cudaStream_t copy_stream = nullptr;     // D2H of phases, overlapped with solves
     cudaEvent_t solved[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
@@ -339,6 +340,7 @@ void free_batch(hs_plan *p)
     dfree(p->d_status); dfree(p->d_degen); dfree(p->d_qstatus);
     dfree(p->d_fields); dfree(p->d_e); dfree(p->d_u); dfree(p->d_inten); dfree(p->d_rel);
     dfree(p->d_out[1]);
+    dfree(p->d_raster);
     dfree(p->d_phase);
     p->d_out[0] = nullptr;
     dfree(p->d_trace_w); dfree(p->d_trace_m);
@@ -363,7 +365,8 @@ int ensure_batch(hs_plan *p, int batch, int n)
         (rc = dalloc(&p->d_coef, bn)) || (rc = dalloc(&p->d_status, B)) || (rc = dalloc(&p->d_degen, B)) ||
         (rc = dalloc(&p->d_qstatus, B)) || (rc = dalloc(&p->d_fields, bn * 2)) || (rc = dalloc(&p->d_e, B)) ||
         (rc = dalloc(&p->d_u, B)) || (rc = dalloc(&p->d_inten, bn)) || (rc = dalloc(&p->d_rel, bn)) ||
-        (rc = dalloc(&p->d_phase, (size_t)B * p->m)) || (rc = dalloc(&p->d_out[1], (size_t)B * p->m))) {
+        (rc = dalloc(&p->d_phase, (size_t)B * p->m)) || (rc = dalloc(&p->d_out[1], (size_t)B * p->m)) ||
+        (rc = dalloc(&p->d_raster, (size_t)B * p->side * p->side))) {
         free_batch(p);
         return rc;
     }
@@ -463,7 +466,8 @@ FoldArgs fold_args(hs_plan *p, int32_t nchunks, const UpdArgs &u, int32_t lo = 0
 }
 
 // Full-range fused pass with the GEMM-tile kernel (n <= 128).
-int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int32_t lo = 0, int32_t hi = -1)
+int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int32_t lo = 0, int32_t hi = -1,
+                unsigned char *raster = nullptr)
 {
     if (hi < 0) hi = p->ntiles;
     const Config &c = p->cfg;
@@ -481,6 +485,7 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     a.idx_img = p->d_idx_img;
     a.phase_out = phase_out;
     a.phase_stride = p->m;
+    a.raster = raster;
     a.f = fold_args(p, p->ntiles, u, lo, hi);
     TileFn fn = hs_select_tile(c.ns, write);
     if (hi <= lo) return HS_OK;
@@ -493,7 +498,7 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
 // One pass over `count` entries of list `l` starting at entry `off`.
 int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t count, int64_t idx_base,
                 const double *phase_in, double *phase_out, int64_t phase_stride, const UpdArgs &u,
-                int32_t lo = 0, int32_t hi = -1)
+                int32_t lo = 0, int32_t hi = -1, unsigned char *raster = nullptr)
 {
     const Config &c = p->cfg;
     const Geom geo = geom_of(l, count, c.spw);
@@ -510,6 +515,8 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
     a.np = c.np;
     a.nl = c.NL;
     a.sorted_rows = l.sorted_rows;
+    a.raster = raster;
+    a.side = p->side;
     a.tab_stride = (int64_t)p->side * c.np;
     a.gx = p->d_gx;
     a.gy = p->d_gy;
@@ -571,9 +578,14 @@ int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags, doub
     const int final_mode = want_fields ? (PM_BWD | PM_FWD | PM_WRITE) : (PM_BWD | PM_WRITE);
     const UpdArgs fin = upd_args(p, want_fields ? ACT_FINAL : ACT_NONE);
     const bool tiled = p->cfg.ns > 0;
+    unsigned char *raster = (flags & HS_WANT_RASTER) ? p->d_raster : nullptr;
+    if (raster)
+        CUDA_TRY(cudaMemsetAsync(raster, 0, (size_t)p->batch * p->side * p->side, p->stream));
     auto full_pass = [&](int mode, const UpdArgs &u) -> int {
-        if (tiled && (mode & PM_FWD)) return launch_tile(p, (mode & PM_WRITE) != 0, u, out);
-        return launch_pass(p, mode, *dense, 0, dense->count, 0, nullptr, (mode & PM_WRITE) ? out : nullptr, m, u);
+        const bool wr = (mode & PM_WRITE) != 0;
+        if (tiled && (mode & PM_FWD)) return launch_tile(p, wr, u, out, 0, -1, wr ? raster : nullptr);
+        return launch_pass(p, mode, *dense, 0, dense->count, 0, nullptr, wr ? out : nullptr, m, u, 0, -1,
+                           wr ? raster : nullptr);
     };
     if (alg == HS_ALG_RS) return full_pass(final_mode, fin);
     const int cs = (subset < m) ? std::max(0, iters - 2) : 0;
@@ -1209,6 +1221,84 @@ int hs_shard_update(hs_plan *p, int j, const double *groups, int ngroups)
     hs_fold_update_kernel<<<p->batch, kThreads, sizeof(double2) * 2 * np, p->stream>>>(fold_args(p, 0, u), ngroups);
     CUDA_TRY(cudaGetLastError());
     if (last) sh.active = false;
+    return sync_and_check(p);
+}
+
+// Standalone SLM raster of a storage-order phase (fileio.py:233-241 with
+// PhaseLut.gray, fileio.py:202-213): linear table in closed form, custom
+// table by first-minimum circular distance, both in fp64 in the reference's
+// operation order.
+static __device__ double hs_wrap_ref(double t)
+{
+    double w = fmod(t, kTwoPi);
+    if (w >= kPi) w = __dadd_rn(w, -kTwoPi);
+    if (w < -kPi) w = __dadd_rn(w, kTwoPi);
+    return w;
+}
+
+static __global__ void hs_raster_kernel(int64_t m, const int32_t *rc, const double *phase, const double *lut,
+                                        int side, unsigned char *out)
+{
+    __shared__ double tab[256];
+    if (lut)
+        for (int k = threadIdx.x; k < 256; k += blockDim.x) tab[k] = lut[k];
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const double p = hs_wrap_ref(phase[i]);
+        unsigned char g;
+        if (!lut) {
+            g = hs_gray_linear(p);
+        } else {
+            double best = INFINITY;
+            int bi = 0;
+            for (int k = 0; k < 256; ++k) {
+                const double d = fabs(hs_wrap_ref(__dadd_rn(p, -tab[k])));
+                if (d < best) {
+                    best = d;
+                    bi = k;
+                }
+            }
+            g = (unsigned char)bi;
+        }
+        const int v = rc[i];
+        out[(int64_t)(v >> 16) * side + (v & 0xffff)] = g;
+    }
+}
+
+int hs_raster(hs_plan *p, const double *phase, const double *lut, unsigned char *out)
+{
+    int rc;
+    if ((rc = check_device(p))) return rc;
+    const size_t cells = (size_t)p->side * p->side;
+    double *d_lut = nullptr, *d_ph = nullptr;
+    unsigned char *d_img = nullptr;
+    if ((lut && (rc = dalloc(&d_lut, 256))) || (rc = dalloc(&d_ph, p->m)) || (rc = dalloc(&d_img, cells))) {
+        dfree(d_lut);
+        dfree(d_ph);
+        return rc;
+    }
+    if (lut) CUDA_TRY(cudaMemcpyAsync(d_lut, lut, sizeof(double) * 256, cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(d_ph, phase, sizeof(double) * p->m, cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemsetAsync(d_img, 0, cells, p->stream));
+    hs_raster_kernel<<<4 * 148, 256, 0, p->stream>>>(p->m, p->storage.rc, d_ph, d_lut, p->side, d_img);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, d_img, cells, cudaMemcpyDeviceToHost, p->stream));
+    rc = sync_and_check(p);
+    dfree(d_lut);
+    dfree(d_ph);
+    dfree(d_img);
+    return rc;
+}
+
+int hs_get_raster(hs_plan *p, int first, int count, unsigned char *out)
+{
+    if (!(p->last_flags & HS_WANT_RASTER)) return fail(HS_EINVAL, "last solve did not build rasters");
+    if (first < 0 || count < 0 || first + count > p->batch) return fail(HS_EINVAL, "pattern range invalid");
+    int rc;
+    if ((rc = check_device(p))) return rc;
+    const size_t cells = (size_t)p->side * p->side;
+    if (count)
+        CUDA_TRY(cudaMemcpyAsync(out, p->d_raster + first * cells, count * cells, cudaMemcpyDeviceToHost, p->stream));
     return sync_and_check(p);
 }
 

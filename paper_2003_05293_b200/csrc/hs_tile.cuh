@@ -37,6 +37,7 @@ struct TileArgs {
     const float *amp_img;     // [side][side], 0 outside the aperture
     const int32_t *idx_img;   // [side][side] storage index, -1 outside
     double *phase_out;        // [B][phase_stride] (WRITE)
+    unsigned char *raster;    // [B][side][side] SLM gray raster (WRITE, nullable)
     int64_t phase_stride;
     FoldArgs f;
 };
@@ -155,6 +156,7 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tile_kernel(const TileArgs a)
                         else if (ph < -kPi) ph += kTwoPi;  // fp32 -pi lies below fp64 -pi
                     }
                     a.phase_out[(int64_t)pat * a.phase_stride + di] = ph;
+                    if (a.raster) a.raster[(int64_t)pat * a.side * a.side + gidx] = hs_gray_linear(ph);
                 }
             }
         }

@@ -148,13 +148,13 @@ class BatchResult:
 
 
 def _run_batch(algorithm: str, pupil: Pupil, spot_sets, iterations: int, subset: int,
-               seeds, fetch_phase: bool = True) -> BatchResult:
+               seeds, fetch_phase: bool = True, raster: bool = False) -> BatchResult:
     plan = _lib.plan_for(pupil)
     plan.set_spots(spot_sets)
     n = plan.n
     theta0 = np.stack([_theta0(int(s), n) for s in seeds])
     iters = 0 if algorithm == "rs" else iterations
-    plan.solve(_ALG_CODE[algorithm], iters, subset, theta0, want_fields=True)
+    plan.solve(_ALG_CODE[algorithm], iters, subset, theta0, want_fields=True, raster=raster)
     status, deg = plan.status()
     w, mg = plan.trace(iters)
     e, u, inten, rel, fields = plan.quality_batch()
@@ -249,7 +249,7 @@ def solve(pupil: Pupil, spots: SpotSet, config: SolverConfig, chunk: int = DEFAU
                  workers=workers)
 
 
-def solve_batch(pupil: Pupil, spot_sets, config: SolverConfig, seeds=None):
+def solve_batch(pupil: Pupil, spot_sets, config: SolverConfig, seeds=None, raster: bool = False):
     """Solve many independent patterns (equal spot counts) in one graph replay.
 
     Returns a list of ``(Hologram, SolverTrace)``; pattern k uses solver seed
@@ -268,7 +268,8 @@ def solve_batch(pupil: Pupil, spot_sets, config: SolverConfig, seeds=None):
     if config.algorithm == "cswgs":
         subset = CompressionPlan.for_pupil(pupil, config.compression).subset_size
     t0 = time.perf_counter()
-    res = _run_batch(config.algorithm, pupil, sets, config.iterations, subset, seeds)
+    res = _run_batch(config.algorithm, pupil, sets, config.iterations, subset, seeds,
+                     raster=raster)
     return [_assemble(config.algorithm, pupil, s, res, b, config.iterations, subset, t0)
             for b, s in enumerate(sets)]
 

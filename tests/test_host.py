@@ -235,3 +235,20 @@ def test_render_validation_before_device(pupils):
     with pytest.raises(hs.InvalidParameterError):
         hs.probe_intensities(p, holo, np.zeros((3, 2)))
     assert hs.probe_intensities(p, holo, np.zeros((0, 3))).shape == (0,)
+
+
+# -------------------------------------------------------------------- LUT
+def test_phase_lut_reference_behaviour(tmp_path):
+    lut = hs.PhaseLut.default()
+    assert lut.table[0] == -math.pi and lut.table[128] == 0.0
+    assert int(lut.gray(math.pi - 1e-9)) == 0
+    for p in np.linspace(-math.pi, math.pi - 1e-12, 997):
+        assert abs(float(hs.wrap_phase(lut.phase(lut.gray(p)) - p))) <= math.pi / 256
+    table = np.linspace(-math.pi, math.pi, 256, endpoint=False)[::-1]
+    path = tmp_path / "lut.txt"
+    path.write_text("\n".join(f"{v:.17g}" for v in table) + "\n")
+    custom = hs.PhaseLut.from_file(path)
+    assert custom.gray(np.array([table[3], table[77]])).tolist() == [3, 77]
+    (tmp_path / "short.txt").write_text("0.0\n0.1\n")
+    with pytest.raises(hs.InvalidParameterError):
+        hs.PhaseLut.from_file(tmp_path / "short.txt")
