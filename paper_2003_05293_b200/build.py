@@ -62,6 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as pool:
         objs = list(pool.map(compile_one, sources()))
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     tmp = LIB + ".tmp"
     subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
                     "-o", tmp, *objs], check=True)

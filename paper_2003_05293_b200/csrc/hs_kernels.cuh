@@ -188,7 +188,7 @@ __device__ __forceinline__ T hs_tree(T *buf, T v, Op op)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
     const int tid = threadIdx.x;
-    if ((tid & 31) == 0) buf[tid >> 5] = v;
+    if ((tid & 31) == 0 && tid < kThreads) buf[tid >> 5] = v;
     __syncthreads();
     T r = buf[0];
 #pragma unroll
@@ -202,12 +202,20 @@ struct DMin { __device__ double operator()(double p, double q) const { return fm
 struct DMax { __device__ double operator()(double p, double q) const { return fmax(p, q); } };
 struct ISum { __device__ int operator()(int p, int q) const { return p + q; } };
 
+// Threads of a CTA that take part in the fold / update arithmetic: the first
+// kThreads (wider CTAs only join the barriers), so every kernel folds and
+// updates with the same reduction order -- bitwise identical results.
+__device__ __forceinline__ int hs_team_tid()
+{
+    return threadIdx.x < kThreads ? (int)threadIdx.x : (1 << 29);
+}
+
 // The pattern's fields E (fp64, in shared memory) -> action.  Runs in the
-// last CTA of the pattern with all kThreads threads.
+// last CTA of the pattern (kThreads team; all threads reach the barriers).
 __device__ __forceinline__ void hs_update(const UpdArgs &a, int b, double2 *E, double *mag_s,
                                        double *dbuf, int *ibuf)
 {
-    const int tid = threadIdx.x;
+    const int tid = hs_team_tid();
     const int n = a.n, np = a.np;
     if (a.act == ACT_FIELDS || a.act == ACT_FINAL) {
         double esum = 0.0, hi = -INFINITY, lo = INFINITY;
@@ -306,7 +314,7 @@ __device__ __forceinline__ void hs_fold(const FoldArgs &a, int pat, int chunk, c
     __shared__ int s_last;
     __shared__ double dbuf[kThreads];
     __shared__ int ibuf[kThreads];
-    const int tid = threadIdx.x;
+    const int tid = hs_team_tid();
     const int np = a.np;
     const int ngroups = (a.nchunks + kGroup - 1) / kGroup;
     const int grp = chunk / kGroup;

@@ -23,6 +23,7 @@
 #include "../../include/holospots_b200.h"
 #include "hs_kernels.cuh"
 #include "hs_tile.cuh"
+#include "hs_slab.cuh"
 #include "hs_win.cuh"
 
 using namespace hs;
@@ -58,6 +59,11 @@ struct DevList {
     int64_t count = 0;
     int32_t chunk_len = 0;  // 0: choose from kTargetChunks
     int32_t sorted_rows = 0;
+    // slab-ordered compressed window (hs_slab_kernel): entries (rc, amp bits)
+    // chunk-major, padded per slab to kSlabL; first column of each chunk's slab
+    int2 *ent = nullptr;
+    int32_t *chunk_c0 = nullptr;
+    int32_t sw = 0;
 };
 
 template <typename T>
@@ -144,9 +150,12 @@ struct hs_plan {
     int32_t *d_tiles = nullptr;           // non-empty 64x32 tiles, packed (r0 << 16) | c0
     int32_t ntiles = 0;
     int win_minb = 2;                     // resident CTAs/SM the window kernel is built for
+    int num_sms = 148;
     DevList storage;                      // storage order
     std::map<int, DevList> dense;         // full range, banded layout per slots-per-warp
-    std::map<std::pair<int64_t, int64_t>, DevList> windows;  // sorted (row, col)
+    // compressed windows keyed (start, count, np): slab-ordered for np <= 128
+    // (np > 0 in the key), else sorted (row, col) for the generic pass kernel
+    std::map<std::tuple<int64_t, int64_t, int>, DevList> windows;
 
     // spot batch
     int batch = 0, n = 0, cap_batch = 0, cap_np = 0;
@@ -209,6 +218,8 @@ void free_list(DevList &l)
     dfree(l.rc);
     dfree(l.amp);
     dfree(l.dst);
+    dfree(l.ent);
+    dfree(l.chunk_c0);
     l.count = 0;
 }
 
@@ -269,29 +280,138 @@ int get_dense(hs_plan *p, int spw, const DevList **out)
     return HS_OK;
 }
 
-// Compressed window: storage range [start, start+count) sorted by (row, col).
+// Compressed window for the slab kernel: storage range [start, start+count)
+// cut into column slabs of hs_slab_width(np) columns.  Inside a slab the
+// row-runs (the window pixels of one grid row, by column) are sorted by
+// length and taken two at a time: the two 16-lane pixel groups of a warp
+// walk the two runs of a duo in lockstep, each run padded with
+// zero-amplitude copies of its last entry to the duo's (even) length, so
+// both groups change row on the same trip (no divergence on the V / flush
+// path) and every pair-trip stays inside one run.  Duos are poured into
+// (chunk, warp, trip) slots of kSlabP trips; a slab's last chunk is padded,
+// so chunks never cross a slab.  Entry index of (chunk q, stream 2w + g,
+// trip t) = q * kSlabL + (2w + g) * kSlabP + t.
+int build_slab_window(hs_plan *p, int64_t start, int64_t count, int np, DevList *out)
+{
+    const int side = p->side;
+    const int sw = hs_slab_width(np, side);
+    std::vector<int64_t> keyed(count);
+    for (int64_t i = 0; i < count; ++i) {
+        const int64_t s = start + i;
+        const int r = p->h_rows[s], c = p->h_cols[s];
+        keyed[i] = ((int64_t)(c / sw) * side + r) * side + c;
+    }
+    std::sort(keyed.begin(), keyed.end());
+    auto entry = [&](int64_t key, bool pad) {  // (row << 16 | slab-local column, amp bits)
+        const int r = (int)((key / side) % side), c = (int)(key % side);
+        int2 e;
+        e.x = pack_rc(r, c % sw);
+        e.y = 0;  // +0.0f
+        if (!pad) {
+            float a = p->h_amp[p->h_index[(int64_t)r * side + c]];
+            memcpy(&e.y, &a, sizeof a);
+        }
+        return e;
+    };
+    std::vector<int2> ent;
+    std::vector<int32_t> c0s;
+    int64_t i = 0;
+    while (i < count) {
+        const int64_t slab = keyed[i] / ((int64_t)side * side);
+        // row-runs of this slab: [begin, end) ranges of keyed
+        std::vector<std::pair<int64_t, int64_t>> runs;
+        while (i < count && keyed[i] / ((int64_t)side * side) == slab) {
+            const int64_t b = i, row = (keyed[i] / side) % side;
+            while (i < count && keyed[i] / ((int64_t)side * side) == slab && (keyed[i] / side) % side == row) ++i;
+            runs.emplace_back(b, i);
+        }
+        std::stable_sort(runs.begin(), runs.end(), [](const std::pair<int64_t, int64_t> &x,
+                                                      const std::pair<int64_t, int64_t> &y) {
+            return x.second - x.first > y.second - y.first;
+        });
+        const size_t base = ent.size();
+        int64_t slot = 0;  // trips poured so far: (chunk, warp, trip) = slot / (8P), ...
+        constexpr int GR = kSlabStreams / kSlabWarps;  // pixel groups per warp
+        auto place = [&](int g, const int2 &e) {
+            const int64_t q = slot / ((int64_t)kSlabWarps * kSlabP);
+            const int w = (int)((slot / kSlabP) % kSlabWarps), t = (int)(slot % kSlabP);
+            const size_t idx = base + (size_t)q * kSlabL + (size_t)(GR * w + g) * kSlabP + t;
+            if (ent.size() <= idx) ent.resize(base + (size_t)(q + 1) * kSlabL, make_int2(-1, 0));
+            ent[idx] = e;
+        };
+        for (size_t k = 0; k < runs.size(); k += GR) {
+            // even length: the kernel takes two pixels of a run per trip
+            const int64_t len = (runs[k].second - runs[k].first + 1) & ~(int64_t)1;
+            for (int64_t t = 0; t < len; ++t, ++slot)
+                for (int g = 0; g < GR; ++g) {
+                    // missing runs of the last group repeat run k (zero amplitude)
+                    const auto &run = runs[k + g < runs.size() ? k + g : k];
+                    const bool real = (k + g < runs.size()) && t < run.second - run.first;
+                    const int64_t key = keyed[std::min(run.first + t, run.second - 1)];
+                    place(g, entry(key, !real));
+                }
+        }
+        // pad the slab's last chunk: each stream repeats its previous entry
+        // (zero amplitude); streams with no entry in a warp segment repeat the
+        // slab's first pixel
+        const size_t total = ent.size() - base;
+        for (size_t idx = 0; idx < total; ++idx) {
+            if (ent[base + idx].x != -1) continue;
+            const size_t t = idx % kSlabP;
+            int2 e = (t > 0) ? ent[base + idx - 1] : entry(keyed[runs[0].first], true);
+            e.y = 0;
+            ent[base + idx] = e;
+        }
+        for (size_t q = base; q < ent.size(); q += kSlabL) c0s.push_back((int32_t)slab * sw);
+    }
+    int r;
+    if ((r = dalloc(&out->ent, ent.size())) || (r = dalloc(&out->chunk_c0, c0s.size()))) return r;
+    if (!ent.empty()) {
+        CUDA_TRY(cudaMemcpy(out->ent, ent.data(), ent.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(out->chunk_c0, c0s.data(), c0s.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    out->count = (int64_t)ent.size();
+    out->chunk_len = kSlabL;
+    out->sorted_rows = 1;
+    out->sw = sw;
+    return HS_OK;
+}
+
+// Compressed window: storage range [start, start+count).  np <= 128: the
+// slab-ordered list of hs_slab_kernel; otherwise sorted by (row, col) for
+// the generic pass kernel.
 int get_window(hs_plan *p, int64_t start, int64_t count, const DevList **out)
 {
-    auto key = std::make_pair(start, count);
+    const int np = p->cfg.ns > 0 ? p->cfg.np : 0;
+    auto key = std::make_tuple(start, count, np);
     auto it = p->windows.find(key);
     if (it == p->windows.end()) {
-        std::vector<int64_t> keyed(count);
-        for (int64_t i = 0; i < count; ++i) {
-            const int64_t s = start + i;
-            keyed[i] = ((int64_t)p->h_rows[s] * p->side + p->h_cols[s]) * p->m + s;
-        }
-        std::sort(keyed.begin(), keyed.end());
-        std::vector<int32_t> rc(count);
-        std::vector<float> amp(count);
-        for (int64_t i = 0; i < count; ++i) {
-            const int64_t s = keyed[i] % p->m;
-            rc[i] = pack_rc(p->h_rows[s], p->h_cols[s]);
-            amp[i] = p->h_amp[s];
-        }
         DevList l;
-        int r = upload_entries(rc, amp, nullptr, 0, &l);
-        if (r) return r;
-        l.sorted_rows = 1;
+        int r;
+        if (np > 0) {
+            r = build_slab_window(p, start, count, np, &l);
+            if (r) {
+                free_list(l);
+                return r;
+            }
+        } else {
+            std::vector<int64_t> keyed(count);
+            for (int64_t i = 0; i < count; ++i) {
+                const int64_t s = start + i;
+                keyed[i] = ((int64_t)p->h_rows[s] * p->side + p->h_cols[s]) * p->m + s;
+            }
+            std::sort(keyed.begin(), keyed.end());
+            std::vector<int32_t> rc(count);
+            std::vector<float> amp(count);
+            for (int64_t i = 0; i < count; ++i) {
+                const int64_t s = keyed[i] % p->m;
+                rc[i] = pack_rc(p->h_rows[s], p->h_cols[s]);
+                amp[i] = p->h_amp[s];
+            }
+            r = upload_entries(rc, amp, nullptr, 0, &l);
+            if (r) return r;
+            l.sorted_rows = 1;
+        }
         it = p->windows.emplace(key, l).first;
     }
     *out = &it->second;
@@ -495,6 +615,45 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     return HS_OK;
 }
 
+// Compressed-window pass over chunks [lo, hi) of a slab-ordered list.  A CTA
+// streams cpc chunks (cpc | kGroup; chunk ranges are group-aligned): the
+// choice minimises waves x (cpc + staging cost) for this batch and never
+// changes results (each chunk keeps its own partial).
+int launch_slab(hs_plan *p, int mode, const DevList &l, int32_t nchunks, const UpdArgs &u, int32_t lo, int32_t hi)
+{
+    const Config &c = p->cfg;
+    if (mode != (PM_BWD | PM_FWD)) return fail(HS_ECUDA, "slab window lists support the fused pass only");
+    if (nchunks > p->cap_chunks) return fail(HS_ECUDA, "fold buffers too small (%d chunks)", nchunks);
+    SlabArgs a;
+    memset(&a, 0, sizeof a);
+    a.ent = l.ent;
+    a.chunk_c0 = l.chunk_c0;
+    a.sw = l.sw;
+    a.side = p->side;
+    a.tab_stride = (int64_t)p->side * c.np;
+    a.gx = p->d_gx;
+    a.gy = p->d_gy;
+    a.coef = p->d_coef;
+    a.f = fold_args(p, nchunks, u, lo, hi);
+    const int64_t span = hi - lo;
+    int best = 1;
+    double best_cost = 1e300;
+    for (int cpc = 1; cpc <= kGroup; cpc *= 2) {
+        const int64_t ctas = (span + cpc - 1) / cpc * p->batch;
+        const int64_t waves = (ctas + p->num_sms - 1) / p->num_sms;
+        const double cost = (double)waves * (std::min<int64_t>(cpc, span) + 0.5);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = cpc;
+        }
+    }
+    a.cpc = best;
+    dim3 grid((unsigned)((span + best - 1) / best), p->batch);
+    hs_select_slab(c.ns)<<<grid, kSlabThreads, hs_slab_smem_bytes(c.np, l.sw), p->stream>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    return HS_OK;
+}
+
 // One pass over `count` entries of list `l` starting at entry `off`.
 int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t count, int64_t idx_base,
                 const double *phase_in, double *phase_out, int64_t phase_stride, const UpdArgs &u,
@@ -526,6 +685,7 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
     a.phase_stride = phase_stride;
     if (hi < 0) hi = geo.nchunks;
     if (hi <= lo) return HS_OK;
+    if (l.sw > 0) return launch_slab(p, mode, l, geo.nchunks, u, lo, hi);
     a.f = fold_args(p, geo.nchunks, u, lo, hi);
     dim3 grid(hi - lo, p->batch);
     if (l.sorted_rows && c.ns > 0 && mode == (PM_BWD | PM_FWD)) {
@@ -713,6 +873,11 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
         CUDA_TRY(cudaMemcpy(p->d_idx_img, p->h_index.data(), cells * sizeof(int32_t), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
         if (const char *env = getenv("HS_WIN_MINB")) p->win_minb = atoi(env);
+        CUDA_TRY(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
+        for (int ns = 1; ns <= 8; ++ns)
+            CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_slab(ns),
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kSlabSmemBudget));  // process-wide cap: never lower it per plan
         for (int ns = 1; ns <= 8; ++ns)
             for (int mb = 2; mb <= 4; ++mb)
                 CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_win(ns, mb),
@@ -775,9 +940,12 @@ int hs_set_spots(hs_plan *p, int batch, int n, const double *x, const double *y,
     p->cfg = pick_config(n);
     const DevList *dense;
     if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
+    // slab windows: one chunk per kSlabL entries plus one padded tail per slab
+    const int64_t slab_chunks =
+        p->cfg.ns > 0 ? p->m / kSlabL + p->side / hs_slab_width(p->cfg.np, p->side) + 2 : 0;
     const int64_t chunks = std::max<int64_t>({(int64_t)geom_of(*dense, dense->count, p->cfg.spw).nchunks,
                                               (int64_t)kTargetChunks + 1, p->m / kMaxChunk + 2,
-                                              (int64_t)p->ntiles});
+                                              (int64_t)p->ntiles, slab_chunks});
     if ((rc = ensure_fold(p, chunks))) return rc;
     const size_t bytes = sizeof(double) * (size_t)batch * n;
     CUDA_TRY(cudaMemcpyAsync(p->d_x, x, bytes, cudaMemcpyHostToDevice, p->stream));

@@ -1,0 +1,22 @@
+// Instantiates the slab-staged compressed-window kernel for NS = 1..8
+// (np = 16 NS <= 128 spots).
+#include "hs_slab.cuh"
+
+namespace hs {
+
+SlabFn hs_select_slab(int ns)
+{
+    switch (ns) {
+    case 1: return hs_slab_kernel<1>;
+    case 2: return hs_slab_kernel<2>;
+    case 3: return hs_slab_kernel<3>;
+    case 4: return hs_slab_kernel<4>;
+    case 5: return hs_slab_kernel<5>;
+    case 6: return hs_slab_kernel<6>;
+    case 7: return hs_slab_kernel<7>;
+    case 8: return hs_slab_kernel<8>;
+    default: return nullptr;
+    }
+}
+
+}  // namespace hs

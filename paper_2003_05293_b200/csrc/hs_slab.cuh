@@ -1,0 +1,423 @@
+// hs_slab.cuh -- compressed-window fused pass with the gx table staged in
+// shared memory (solver iterations 1..I-2, solvers.py:212-230).
+//
+// A window is a random 1/16 of the aperture (a storage-order range of the
+// seeded permutation, optics.py:184-187), so the gx row a pixel needs is a
+// random row of the pattern's table.  Gathering those rows from L2 made the
+// window pass latency-bound (hs_win.cuh).  Here the grid is cut into column
+// slabs of `sw` columns whose gx rows fit in shared memory (sw * np * 8 B,
+// ~200 KB); the window list is ordered (slab, row, col) and cut into chunks
+// of 32 streams x P entries that never cross a slab.  A CTA
+//
+//   * stages its slab's gx rows with one TMA bulk copy (cp.async.bulk, an
+//     mbarrier with the byte count) -- re-staged only when its next chunk
+//     lies in another slab;
+//   * runs 32 independent pixel streams, 8 lanes per pixel, lane g owning
+//     spots {2(g+8j), 2(g+8j)+1}: each pixel reads its gx row from shared
+//     memory as float4 (one 128-B wavefront per 8-lane group, conflict-free);
+//   * keeps V = coef * gy[row] and T = sum_p b_p gx[c_p] per row in
+//     registers (the row-run scheme of hs_pass_kernel), E in registers;
+//   * prefetches the gy row of the entry three ahead into L1 and loads the
+//     entry stream five ahead, so row changes do not stall on L2.
+//
+// Per pixel-spot pair: one 8-B shared-memory read + 8 FFMA (backward
+// kernels.py:99-119, forward kernels.py:122-144).  Each chunk's partial is the
+// 8 warps' E summed in warp order; chunks are folded by hs_fold -- the
+// reduction shape depends only on the list, so results are bitwise
+// independent of the batch size and of how many chunks a CTA streams.
+#pragma once
+
+#include "hs_kernels.cuh"
+
+namespace hs {
+
+constexpr int kSlabThreads = 512;                // 16 warps
+constexpr int kSlabWarps = kSlabThreads / 32;
+constexpr int kSlabStreams = 32;                 // 16 warps x 2 pixel groups of 16 lanes
+constexpr int kSlabP = 16;                       // entries per stream per chunk
+constexpr int kSlabL = kSlabStreams * kSlabP;    // entries per chunk
+constexpr int kSlabSmemBudget = 220 * 1024;      // dynamic smem cap per CTA
+constexpr int kBulkPiece = 32 * 1024;            // bytes per cp.async.bulk
+
+struct SlabArgs {
+    const int2 *ent;          // (rc, amp bits) per entry, chunk-major, padded to kSlabL
+    const int32_t *chunk_c0;  // first grid column of each chunk's slab
+    int32_t sw;               // slab width (columns)
+    int32_t side;
+    int32_t cpc;              // chunks per CTA (divides kGroup)
+    int64_t tab_stride;       // side * np
+    const float2 *gx, *gy;    // [B][side][np]
+    const float2 *coef;       // [B][np]
+    FoldArgs f;
+};
+
+__host__ __device__ constexpr size_t hs_slab_fixed_bytes(int np)
+{
+    // per-stream E [32][np] float2 + entries [2][kSlabL] int2 + coef [np] float2
+    return (size_t)kSlabStreams * np * 8 + (size_t)2 * kSlabL * 8 + (size_t)np * 8;
+}
+
+// Widest slab whose gx rows fit next to the per-CTA scratch.
+__host__ __device__ constexpr int hs_slab_width(int np, int side)
+{
+    return ((int)((kSlabSmemBudget - hs_slab_fixed_bytes(np)) / (sizeof(float2) * np)) & ~7) < side
+               ? ((int)((kSlabSmemBudget - hs_slab_fixed_bytes(np)) / (sizeof(float2) * np)) & ~7)
+               : side;
+}
+
+__host__ __device__ constexpr size_t hs_slab_smem_bytes(int np, int sw)
+{
+    return sizeof(float2) * (size_t)np * sw + hs_slab_fixed_bytes(np);
+}
+
+__device__ __forceinline__ uint32_t hs_smem_addr(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ float4 hs_lds4(uint32_t addr)
+{
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ void hs_sts4(uint32_t addr, float4 v)
+{
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ int2 hs_lds2i(uint32_t addr)
+{
+    int2 v;
+    asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ float hs_rsqrt(float x)
+{
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// b = A conj(S)/|S| with arg(0) = 0 (kernels.py:136-137, solvers.py:96-101)
+__device__ __forceinline__ void hs_bvec(float sr, float si, float A, float &br, float &bi)
+{
+    const float m2 = fmaf(sr, sr, si * si);
+    if (__float_as_uint(m2) - 0x0d800000u < 0x64000000u) {  // 2^-100 <= m2 < 2^100
+        const float inv = A * hs_rsqrt(m2);
+        br = sr * inv;
+        bi = -si * inv;
+    } else if (sr != 0.f || si != 0.f) {
+        const float mx = fmaxf(fabsf(sr), fabsf(si));
+        const float xr = sr / mx, xi = si / mx;
+        const float inv = A * hs_rsqrt(fmaf(xr, xr, xi * xi));
+        br = xr * inv;
+        bi = -xi * inv;
+    } else {
+        br = A;
+        bi = 0.f;
+    }
+}
+
+__device__ __forceinline__ float2 hs_lds2(uint32_t addr)
+{
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ void hs_sts2(uint32_t addr, float2 v)
+{
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs a)
+{
+    constexpr int NP = 16 * NS;
+    constexpr int P = kSlabP;
+    extern __shared__ float4 sm4[];
+    __shared__ __align__(8) unsigned long long bar;
+
+    const int pat = blockIdx.y;
+    if (a.f.u.status[pat] != 0) return;
+    const int q0 = a.f.chunk_base + blockIdx.x * a.cpc;
+    const int nq = min(a.cpc, a.f.chunk_end - q0);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int g = lane & 15, s = lane >> 4;
+    const bool lo = g < 8;
+    const int stream = warp * 2 + s;
+
+    float2 *Xs = reinterpret_cast<float2 *>(sm4);                 // [sw][NP]
+    float2 *Es = Xs + (size_t)a.sw * NP;                            // [32][NP]
+    int2 *Ent = reinterpret_cast<int2 *>(Es + kSlabStreams * NP);   // [2][kSlabL]
+    float2 *coef_s = reinterpret_cast<float2 *>(Ent + 2 * kSlabL);  // [NP]
+    const uint32_t xs_a = hs_smem_addr(Xs) + 8u * g;
+    const uint32_t es_a = hs_smem_addr(Es) + 8u * (stream * NP + g);
+    const uint32_t ent_a = hs_smem_addr(Ent);
+    const uint32_t cf_a = hs_smem_addr(coef_s) + 8u * g;
+
+    for (int k = tid; k < NP; k += kSlabThreads) coef_s[k] = a.coef[(int64_t)pat * NP + k];
+    for (int k = tid; k < kSlabStreams * NP; k += kSlabThreads) Es[k] = make_float2(0.f, 0.f);
+
+    // per-warp entry staging: the warp's 2 streams of chunk q are the 2P
+    // entries [2 w P, 2 (w+1) P) of the chunk -- one int2 per lane
+    static_assert(2 * kSlabP == 32, "one entry per lane per warp segment");
+    int2 ent_reg = make_int2(0, 0);
+    auto fetch_ent = [&](int qi) {
+        if (qi < nq) ent_reg = __ldg(a.ent + (int64_t)(q0 + qi) * kSlabL + warp * 2 * P + lane);
+    };
+    auto store_ent = [&](int qi) {
+        if (qi < nq) Ent[(qi & 1) * kSlabL + warp * 2 * P + lane] = ent_reg;
+    };
+    fetch_ent(0);
+    store_ent(0);
+    fetch_ent(1);
+    store_ent(1);
+    const uint32_t bar_a = hs_smem_addr(&bar);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const float2 *__restrict__ gx = a.gx + (int64_t)pat * a.tab_stride;
+    const float2 *__restrict__ Y = a.gy + (int64_t)pat * a.tab_stride + g;
+    uint32_t phase = 0;
+    int c0 = -1;
+
+    // Stage the gx rows of slab [cs, cs + sw) (all threads call; one issues).
+    auto stage = [&](int cs) {
+        __syncthreads();  // previous readers of Xs are done
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const int ncol = min(a.sw, a.side - cs);
+            const uint32_t bytes = (uint32_t)ncol * NP * 8u;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a), "r"(bytes)
+                         : "memory");
+            const char *src = reinterpret_cast<const char *>(gx + (int64_t)cs * NP);
+            const uint32_t dst = hs_smem_addr(Xs);
+            for (uint32_t off = 0; off < bytes; off += kBulkPiece) {
+                const uint32_t len = min((uint32_t)kBulkPiece, bytes - off);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        dst + off),
+                    "l"(src + off), "r"(len), "r"(bar_a)
+                    : "memory");
+            }
+        }
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                : "=r"(done)
+                : "r"(bar_a), "r"(phase)
+                : "memory");
+        }
+        phase ^= 1u;
+        c0 = cs;
+    };
+
+    // lane state: spots g + 16 j, j < NS
+    float vr[NS], vi[NS], yr_[NS], yi_[NS], tr[NS], ti[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) vr[k] = vi[k] = yr_[k] = yi_[k] = tr[k] = ti[k] = 0.f;
+
+    auto ent_pair = [&](int qi, int t) -> int4 {  // entries t, t+1 (t even) of this stream
+        int4 v;
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(ent_a + 8u * ((qi & 1) * kSlabL + stream * P + t)));
+        return v;
+    };
+    auto load_x = [&](int rc, float (&xr)[NS], float (&xi)[NS]) {
+        const uint32_t row = xs_a + 8u * NP * (uint32_t)(rc & 0xffff);  // slab-local column
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            const float2 q = hs_lds2(row + 128u * j);
+            xr[j] = q.x;
+            xi[j] = q.y;
+        }
+    };
+    auto flush = [&]() {  // Es[stream] += Y * T ; T = 0
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            float2 e = hs_lds2(es_a + 128u * j);
+            e.x = fmaf(yr_[j], tr[j], e.x);
+            e.x = fmaf(-yi_[j], ti[j], e.x);
+            e.y = fmaf(yr_[j], ti[j], e.y);
+            e.y = fmaf(yi_[j], tr[j], e.y);
+            tr[j] = 0.f;
+            ti[j] = 0.f;
+            hs_sts2(es_a + 128u * j, e);
+        }
+    };
+    auto set_row = [&](const float2 (&yq)[NS]) {  // Y = row, V = coef * Y
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            const float2 q = yq[j];
+            const float2 w = hs_lds2(cf_a + 128u * j);
+            yr_[j] = q.x;
+            yi_[j] = q.y;
+            vr[j] = fmaf(w.x, q.x, -w.y * q.y);
+            vi[j] = fmaf(w.x, q.y, w.y * q.x);
+        }
+    };
+    auto load_y = [&](int r, float2 (&yq)[NS]) {
+        const float2 *yrow = Y + (int64_t)r * NP;
+#pragma unroll
+        for (int j = 0; j < NS; ++j) yq[j] = __ldg(yrow + 16 * j);
+    };
+    // T += b x for one pixel; each part of b feeds NS consecutive FFMAs
+    auto fwd = [&](const float (&xr)[NS], const float (&xi)[NS], float br, float bi) {
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            tr[k] = fmaf(br, xr[k], tr[k]);
+            ti[k] = fmaf(br, xi[k], ti[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            tr[k] = fmaf(-bi, xi[k], tr[k]);
+            ti[k] = fmaf(bi, xr[k], ti[k]);
+        }
+    };
+
+    __syncwarp();
+    stage(__ldg(a.chunk_c0 + q0));
+    int rcur = -1;
+    float2 yn[NS];  // gy row of the stream's next run, loaded ahead of use
+    int yn_row = -1;
+    constexpr int DP = 2;  // lookahead in pairs
+    int4 en = ent_pair(0, 0);
+
+    // One pair-trip = two pixels per 16-lane group (entries t, t+1 of a run;
+    // runs are padded to even length, so both share the row).
+    auto pair = [&](int qi, int t) {
+        const int4 e = en;
+        float xar[NS], xai[NS], xbr[NS], xbi[NS];
+        load_x(e.x, xar, xai);
+        load_x(e.z, xbr, xbi);
+        {
+            const int tn = t + 2, qn = qi + (tn >= P);
+            if (qn < nq) en = ent_pair(qn, tn - (tn >= P ? P : 0));
+            const int tp = t + 2 * DP, qp = qi + (tp >= P);
+            if (qp < nq && yn_row < 0) {
+                const int rp = ent_pair(qp, tp - (tp >= P ? P : 0)).x >> 16;
+                if (rp != (e.x >> 16)) {
+                    load_y(rp, yn);
+                    yn_row = rp;
+                }
+            }
+        }
+        const int r = e.x >> 16;
+        if (r != rcur) {  // warp-uniform: the 2 runs of a duo change row together
+            if (rcur >= 0) flush();
+            if (r == yn_row) {
+                set_row(yn);
+                yn_row = -1;
+            } else {
+                float2 yq[NS];
+                load_y(r, yq);
+                set_row(yq);
+            }
+            rcur = r;
+        }
+        // backward partials of both pixels; V operands feed 4 consecutive FFMAs
+        float ar = 0.f, ai = 0.f, br = 0.f, bi = 0.f;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            ar = fmaf(vr[k], xar[k], ar);
+            ai = fmaf(vr[k], xai[k], ai);
+            br = fmaf(vr[k], xbr[k], br);
+            bi = fmaf(vr[k], xbi[k], bi);
+            ar = fmaf(-vi[k], xai[k], ar);
+            ai = fmaf(vi[k], xar[k], ai);
+            br = fmaf(-vi[k], xbi[k], br);
+            bi = fmaf(vi[k], xbr[k], bi);
+        }
+        // transpose-reduce over the 16 lanes: lanes g < 8 finish pixel A,
+        // lanes g >= 8 pixel B (commutative butterflies: identical bits in
+        // every lane of a half)
+        float kr = lo ? ar : br, ki = lo ? ai : bi;
+        kr += __shfl_xor_sync(0xffffffffu, lo ? br : ar, 8);
+        ki += __shfl_xor_sync(0xffffffffu, lo ? bi : ai, 8);
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            kr += __shfl_xor_sync(0xffffffffu, kr, o);
+            ki += __shfl_xor_sync(0xffffffffu, ki, o);
+        }
+        float mr, mi;
+        hs_bvec(kr, ki, __int_as_float(lo ? e.y : e.w), mr, mi);
+        const float orr = __shfl_xor_sync(0xffffffffu, mr, 8);
+        const float oi = __shfl_xor_sync(0xffffffffu, mi, 8);
+        fwd(xar, xai, lo ? mr : orr, lo ? mi : oi);
+        fwd(xbr, xbi, lo ? orr : mr, lo ? oi : mi);
+    };
+
+    // End of chunk qi: flush, sum the 32 streams in order, reset, stage.
+    auto chunk_end = [&](int qi) {
+        if (rcur >= 0) flush();
+        rcur = -1;
+        __syncthreads();
+        float2 *out = a.f.partials + (int64_t)pat * a.f.part_stride + (int64_t)(q0 + qi) * NP;
+        // streams 2w, 2w+1 of warp w: symmetric add by shuffle, kept in
+        // stream 2w's row; then the 16 warp rows summed in warp order
+        {
+            const uint32_t w0 = hs_smem_addr(Es) + 8u * (2 * warp * NP + g);
+#pragma unroll
+            for (int j = 0; j < NS; ++j) {
+                const float2 v = hs_lds2(es_a + 128u * j);
+                float2 o;
+                o.x = v.x + __shfl_xor_sync(0xffffffffu, v.x, 16);
+                o.y = v.y + __shfl_xor_sync(0xffffffffu, v.y, 16);
+                if (s == 0) hs_sts2(w0 + 128u * j, o);
+                else hs_sts2(es_a + 128u * j, make_float2(0.f, 0.f));
+            }
+        }
+        __syncthreads();
+        for (int k = tid; k < NP; k += kSlabThreads) {
+            float x = 0.f, y = 0.f;
+#pragma unroll
+            for (int w = 0; w < kSlabWarps; ++w) {
+                const float2 v = Es[2 * w * NP + k];
+                x += v.x;
+                y += v.y;
+            }
+            out[k] = make_float2(x, y);
+#pragma unroll
+            for (int w = 0; w < kSlabWarps; ++w) Es[2 * w * NP + k] = make_float2(0.f, 0.f);
+        }
+        store_ent(qi + 2);  // chunk qi's buffer is consumed
+        __syncwarp();
+        if (qi + 1 < nq) {
+            const int cs = __ldg(a.chunk_c0 + q0 + qi + 1);
+            if (cs != c0)
+                stage(cs);        // begins with __syncthreads
+            else
+                __syncthreads();  // Es reset visible before the next flushes
+        }
+    };
+
+    for (int qi = 0; qi < nq; ++qi) {
+        fetch_ent(qi + 2);
+#pragma unroll 1
+        for (int t = 0; t < P; t += 4) {
+            pair(qi, t);
+            pair(qi, t + 2);
+        }
+        chunk_end(qi);
+    }
+    if (a.f.u.act != ACT_NONE) {
+        __syncthreads();
+        hs_fold(a.f, pat, q0, reinterpret_cast<char *>(Es), nq);
+    }
+}
+
+typedef void (*SlabFn)(SlabArgs);
+SlabFn hs_select_slab(int ns);
+
+}  // namespace hs
