@@ -283,17 +283,20 @@ def run_ours(args):
     for p, _ in bufs.values():
         lib.hs_host_free(p)
 
-    # roofline of the dominant kernel: the full-range fused pass
+    # roofline of the dominant kernel (the compressed-window pass: 19 of the
+    # 22 launches, ~57% of the step) and of the full-range pass, each timed
+    # live with CUDA events on the plan stream (hs_time_kernel)
     ms_full, pairs_full = plan.time_kernel(0, reps=10)
     ms_win, pairs_win = plan.time_kernel(1, subset, reps=50)
-    flops_full = 2 * FLOP_PER_PAIR_PASS * pairs_full
-    achieved = flops_full / (ms_full * 1e-3) / 1e12
     peak = _lib.fma_peak_tflops(local)
-    traffic = None
+    flops_win = 2 * FLOP_PER_PAIR_PASS * pairs_win     # backward + forward per pair
+    flops_full = 2 * FLOP_PER_PAIR_PASS * pairs_full
+    achieved_win = flops_win / (ms_win * 1e-3) / 1e12
+    achieved_full = flops_full / (ms_full * 1e-3) / 1e12
+    traffic = {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("full_pass_dram_bytes_per_launch")
-    # per-step composition of kernel time (from the same per-launch timings)
+        traffic = json.load(open(tpath))
     n_full, n_win = 2, ITERS - 1
     step_kernel_ms = n_full * ms_full + n_win * ms_win
 
@@ -317,13 +320,23 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps, "matches_device_e": e2e_ok,
                 "path": "hs_solve_host_async (C ABI, pinned host buffers, phase f64 storage "
                         "order; D2H of step k overlaps the solve of step k+1)"},
-        "roofline": {"bound": "fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "hs_tile_kernel<7,false> full-range fused pass (GEMM tiles) + fold",
-                     "peak_source": "measured FP32 FFMA microbenchmark (hs_fma_peak)",
-                     "algorithmic_flop_per_launch": flops_full,
-                     "ms_per_launch": ms_full,
-                     "window_pass_ms": ms_win,
+        "roofline": {"bound": "fma", "achieved": achieved_win, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved_win / peak,
+                     "traffic": traffic.get("window_pass_dram_bytes_per_launch"),
+                     "kernel": "hs_slab_kernel<7> compressed-window fused pass (backward + "
+                               "forward + fold/update), dominant: 19 of 22 launches per step",
+                     "peak_source": "measured FP32 FFMA microbenchmark (hs_fma_peak, "
+                                    "MEASURED_PEAKS.json has no FP32 figure)",
+                     "algorithmic_flop_per_launch": flops_win,
+                     "flop_per_unit": 16, "unit_def": "pixel-spot pair (backward + forward "
+                     "complex MAC, SURVEY 8(d)); units per launch = S * N * B",
+                     "ms_per_launch": ms_win,
+                     "step_share_estimate": n_win * ms_win / step_kernel_ms,
+                     "full_pass": {"kernel": "hs_tile_kernel<13,false> 64x64-pixel GEMM tiles",
+                                   "ms_per_launch": ms_full, "achieved": achieved_full,
+                                   "frac": achieved_full / peak,
+                                   "algorithmic_flop_per_launch": flops_full,
+                                   "traffic": traffic.get("full_pass_dram_bytes_per_launch")},
                      "step_kernel_ms_estimate": step_kernel_ms},
         "pixel_spot_pairs_per_step": pairs_step,
         "gpu_launches": launches_per_step * args.steps,

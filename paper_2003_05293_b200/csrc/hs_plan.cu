@@ -607,10 +607,12 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     a.phase_stride = p->m;
     a.raster = raster;
     a.f = fold_args(p, p->ntiles, u, lo, hi);
-    TileFn fn = hs_select_tile(c.ns, write);
+    a.n = p->n;
+    const int spt = (p->n + 7) / 8;
+    TileFn fn = hs_select_tile(spt, write);
     if (hi <= lo) return HS_OK;
     dim3 grid(hi - lo, p->batch);
-    fn<<<grid, kThreads, hs_tile_smem_bytes(c.ns), p->stream>>>(a);
+    fn<<<grid, kThreads, hs_tile_smem_bytes(spt, p->n), p->stream>>>(a);
     CUDA_TRY(cudaGetLastError());
     return HS_OK;
 }
@@ -882,11 +884,11 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
             for (int mb = 2; mb <= 4; ++mb)
                 CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_win(ns, mb),
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs_win_smem_bytes(ns)));
-        for (int ns = 1; ns <= 8; ++ns)
+        for (int spt = 1; spt <= 16; ++spt)
             for (int w = 0; w < 2; ++w)
-                CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_tile(ns, w != 0),
+                CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_tile(spt, w != 0),
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)hs_tile_smem_bytes(ns)));
+                                              (int)hs_tile_smem_bytes(spt, 8 * spt)));
     }
     const int modes[4] = {PM_BWD | PM_WRITE, PM_FWD, PM_BWD | PM_FWD, PM_BWD | PM_FWD | PM_WRITE};
     const int gs[6] = {1, 2, 4, 8, 16, 32};
