@@ -27,6 +27,7 @@
 // independent of the batch size and of how many chunks a CTA streams.
 #pragma once
 
+#include "hs_f2.cuh"
 #include "hs_kernels.cuh"
 
 namespace hs {
@@ -222,10 +223,14 @@ __global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs
         c0 = cs;
     };
 
-    // lane state: spots g + 16 j, j < NS
-    float vr[NS], vi[NS], yr_[NS], yi_[NS], tr[NS], ti[NS];
+    // lane state: spots g + 16 j, j < NS; complex values packed (re, im)
+    float vr[NS], vi[NS], yr_[NS], yi_[NS];
+    f2x tt[NS];
 #pragma unroll
-    for (int k = 0; k < NS; ++k) vr[k] = vi[k] = yr_[k] = yi_[k] = tr[k] = ti[k] = 0.f;
+    for (int k = 0; k < NS; ++k) {
+        vr[k] = vi[k] = yr_[k] = yi_[k] = 0.f;
+        tt[k] = 0ull;
+    }
 
     auto ent_pair = [&](int qi, int t) -> int4 {  // entries t, t+1 (t even) of this stream
         int4 v;
@@ -234,26 +239,19 @@ __global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs
                      : "r"(ent_a + 8u * ((qi & 1) * kSlabL + stream * P + t)));
         return v;
     };
-    auto load_x = [&](int rc, float (&xr)[NS], float (&xi)[NS]) {
+    auto load_x = [&](int rc, f2x (&x)[NS]) {
         const uint32_t row = xs_a + 8u * NP * (uint32_t)(rc & 0xffff);  // slab-local column
 #pragma unroll
-        for (int j = 0; j < NS; ++j) {
-            const float2 q = hs_lds2(row + 128u * j);
-            xr[j] = q.x;
-            xi[j] = q.y;
-        }
+        for (int j = 0; j < NS; ++j) asm volatile("ld.shared.b64 %0, [%1];" : "=l"(x[j]) : "r"(row + 128u * j));
     };
     auto flush = [&]() {  // Es[stream] += Y * T ; T = 0
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
-            float2 e = hs_lds2(es_a + 128u * j);
-            e.x = fmaf(yr_[j], tr[j], e.x);
-            e.x = fmaf(-yi_[j], ti[j], e.x);
-            e.y = fmaf(yr_[j], ti[j], e.y);
-            e.y = fmaf(yi_[j], tr[j], e.y);
-            tr[j] = 0.f;
-            ti[j] = 0.f;
-            hs_sts2(es_a + 128u * j, e);
+            f2x e;
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(e) : "r"(es_a + 128u * j));
+            f2_cmac(e, yr_[j], yi_[j], tt[j]);
+            tt[j] = 0ull;
+            asm volatile("st.shared.b64 [%0], %1;" ::"r"(es_a + 128u * j), "l"(e) : "memory");
         }
     };
     auto set_row = [&](const float2 (&yq)[NS]) {  // Y = row, V = coef * Y
@@ -272,19 +270,6 @@ __global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs
 #pragma unroll
         for (int j = 0; j < NS; ++j) yq[j] = __ldg(yrow + 16 * j);
     };
-    // T += b x for one pixel; each part of b feeds NS consecutive FFMAs
-    auto fwd = [&](const float (&xr)[NS], const float (&xi)[NS], float br, float bi) {
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            tr[k] = fmaf(br, xr[k], tr[k]);
-            ti[k] = fmaf(br, xi[k], ti[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            tr[k] = fmaf(-bi, xi[k], tr[k]);
-            ti[k] = fmaf(bi, xr[k], ti[k]);
-        }
-    };
 
     __syncwarp();
     stage(__ldg(a.chunk_c0 + q0));
@@ -293,14 +278,18 @@ __global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs
     int yn_row = -1;
     constexpr int DP = 2;  // lookahead in pairs
     int4 en = ent_pair(0, 0);
+    // pixel roles: lanes g < 8 finish pixel t ("mine") and send t+1's partial,
+    // lanes g >= 8 the reverse -- so the transpose-reduce needs no selects
 
     // One pair-trip = two pixels per 16-lane group (entries t, t+1 of a run;
     // runs are padded to even length, so both share the row).
     auto pair = [&](int qi, int t) {
         const int4 e = en;
-        float xar[NS], xai[NS], xbr[NS], xbi[NS];
-        load_x(e.x, xar, xai);
-        load_x(e.z, xbr, xbi);
+        const int rc_m = lo ? e.x : e.z, rc_o = lo ? e.z : e.x;
+        const float A_m = __int_as_float(lo ? e.y : e.w);
+        f2x xm[NS], xo[NS];
+        load_x(rc_m, xm);
+        load_x(rc_o, xo);
         {
             const int tn = t + 2, qn = qi + (tn >= P);
             if (qn < nq) en = ent_pair(qn, tn - (tn >= P ? P : 0));
@@ -326,36 +315,32 @@ __global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs
             }
             rcur = r;
         }
-        // backward partials of both pixels; V operands feed 4 consecutive FFMAs
-        float ar = 0.f, ai = 0.f, br = 0.f, bi = 0.f;
+        // backward partials of both pixels over this lane's spots (FFMA2)
+        f2x m0 = 0ull, m1 = 0ull, o0 = 0ull, o1 = 0ull;
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
-            ar = fmaf(vr[k], xar[k], ar);
-            ai = fmaf(vr[k], xai[k], ai);
-            br = fmaf(vr[k], xbr[k], br);
-            bi = fmaf(vr[k], xbi[k], bi);
-            ar = fmaf(-vi[k], xai[k], ar);
-            ai = fmaf(vi[k], xar[k], ai);
-            br = fmaf(-vi[k], xbi[k], br);
-            bi = fmaf(vi[k], xbr[k], bi);
+            f2_cmac((k & 1) ? m1 : m0, vr[k], vi[k], xm[k]);
+            f2_cmac((k & 1) ? o1 : o0, vr[k], vi[k], xo[k]);
         }
-        // transpose-reduce over the 16 lanes: lanes g < 8 finish pixel A,
-        // lanes g >= 8 pixel B (commutative butterflies: identical bits in
-        // every lane of a half)
-        float kr = lo ? ar : br, ki = lo ? ai : bi;
-        kr += __shfl_xor_sync(0xffffffffu, lo ? br : ar, 8);
-        ki += __shfl_xor_sync(0xffffffffu, lo ? bi : ai, 8);
+        float kr = f2_lo(m0) + f2_lo(m1), ki = f2_hi(m0) + f2_hi(m1);
+        const float sr_o = f2_lo(o0) + f2_lo(o1), si_o = f2_hi(o0) + f2_hi(o1);
+        // transpose-reduce over the 16 lanes (commutative butterflies: every
+        // lane of a half ends with identical bits)
+        kr += __shfl_xor_sync(0xffffffffu, sr_o, 8);
+        ki += __shfl_xor_sync(0xffffffffu, si_o, 8);
 #pragma unroll
         for (int o = 4; o > 0; o >>= 1) {
             kr += __shfl_xor_sync(0xffffffffu, kr, o);
             ki += __shfl_xor_sync(0xffffffffu, ki, o);
         }
         float mr, mi;
-        hs_bvec(kr, ki, __int_as_float(lo ? e.y : e.w), mr, mi);
+        hs_bvec(kr, ki, A_m, mr, mi);
         const float orr = __shfl_xor_sync(0xffffffffu, mr, 8);
         const float oi = __shfl_xor_sync(0xffffffffu, mi, 8);
-        fwd(xar, xai, lo ? mr : orr, lo ? mi : oi);
-        fwd(xbr, xbi, lo ? orr : mr, lo ? oi : mi);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) f2_cmac(tt[k], mr, mi, xm[k]);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) f2_cmac(tt[k], orr, oi, xo[k]);
     };
 
     // End of chunk qi: flush, sum the 32 streams in order, reset, stage.

@@ -21,6 +21,7 @@
 // partial is folded by the fixed-order two-level tree (hs_fold).
 #pragma once
 
+#include "hs_f2.cuh"
 #include "hs_kernels.cuh"
 
 namespace hs {
@@ -96,50 +97,78 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tile_kernel(const TileArgs a)
     const float2 *gy = a.gy + (int64_t)pat * a.tab_stride;
     const float2 *cf = a.coef + (int64_t)pat * a.np;
 
-    // ---- stage X[k][c] (k < KP) and V[k][r] = coef_k gy[r][k] (k < kb); reads coalesced over k
-    for (int idx = tid; idx < KP * kTileC; idx += kThreads) {
-        const int c = idx / KP, k = idx - c * KP;
-        const int cc = min(c0 + c, a.side - 1);
-        Xs[k * kXS + c] = __ldg(gx + (int64_t)cc * a.np + k);
-    }
-    for (int idx = tid; idx < kb * kTileR; idx += kThreads) {
-        const int r = idx / kb, k = idx - r * kb;
-        const int rr = min(r0 + r, a.side - 1);
-        const float2 q = __ldg(gy + (int64_t)rr * a.np + k);
-        const float2 w = __ldg(cf + k);
-        Vs[k * kVS + r] = make_float2(fmaf(w.x, q.x, -w.y * q.y), fmaf(w.x, q.y, w.y * q.x));
+    // ---- stage X[k][c] (k < KP) and V[k][r] = coef_k gy[r][k] (k < kb).
+    // Warp w takes columns / rows w + 8 i; lane l spots l + 32 m.  All of a
+    // thread's global loads are issued before its shared stores (deep MLP).
+    {
+        constexpr int MK = (KP + 31) / 32;
+        const int lane = tid & 31, warp = tid >> 5;
+        float2 v[8][MK];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float2 *src = gx + (int64_t)min(c0 + warp + 8 * i, a.side - 1) * a.np;
+#pragma unroll
+            for (int m = 0; m < MK; ++m) {
+                const int k = lane + 32 * m;
+                v[i][m] = (k < KP) ? __ldg(src + k) : make_float2(0.f, 0.f);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int m = 0; m < MK; ++m) {
+                const int k = lane + 32 * m;
+                if (k < KP) Xs[k * kXS + warp + 8 * i] = v[i][m];
+            }
+        float2 w[MK];
+#pragma unroll
+        for (int m = 0; m < MK; ++m) {
+            const int k = lane + 32 * m;
+            w[m] = (k < kb) ? __ldg(cf + k) : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float2 *src = gy + (int64_t)min(r0 + warp + 8 * i, a.side - 1) * a.np;
+#pragma unroll
+            for (int m = 0; m < MK; ++m) {
+                const int k = lane + 32 * m;
+                v[i][m] = (k < kb) ? __ldg(src + k) : make_float2(0.f, 0.f);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int m = 0; m < MK; ++m) {
+                const int k = lane + 32 * m;
+                const float2 q = v[i][m];
+                if (k < kb)
+                    Vs[k * kVS + warp + 8 * i] =
+                        make_float2(fmaf(w[m].x, q.x, -w[m].y * q.y), fmaf(w[m].x, q.y, w[m].y * q.x));
+            }
     }
     __syncthreads();
 
     // ---- backward: thread (tr, tc) holds rows 4 tr + i, columns tc + 16 j
     const int tr = tid >> 4, tc = tid & 15;
-    float sr[4][4], si[4][4];
+    f2x sacc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) sr[i][j] = si[i][j] = 0.f;
+        for (int j = 0; j < 4; ++j) sacc[i][j] = 0ull;
+    const f2x *X2 = reinterpret_cast<const f2x *>(Xs);
 #pragma unroll 2
     for (int k = 0; k < kb; ++k) {
         const float4 v01 = *reinterpret_cast<const float4 *>(Vs + k * kVS + 4 * tr);
         const float4 v23 = *reinterpret_cast<const float4 *>(Vs + k * kVS + 4 * tr + 2);
-        float2 x[4];
+        f2x x[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) x[j] = Xs[k * kXS + tc + 16 * j];
+        for (int j = 0; j < 4; ++j) x[j] = X2[k * kXS + tc + 16 * j];
         const float vr[4] = {v01.x, v01.z, v23.x, v23.z};
         const float vi[4] = {v01.y, v01.w, v23.y, v23.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                sr[i][j] = fmaf(vr[i], x[j].x, sr[i][j]);
-                si[i][j] = fmaf(vr[i], x[j].y, si[i][j]);
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                sr[i][j] = fmaf(-vi[i], x[j].y, sr[i][j]);
-                si[i][j] = fmaf(vi[i], x[j].x, si[i][j]);
-            }
-        }
+            for (int j = 0; j < 4; ++j) f2_cmac(sacc[i][j], vr[i], vi[i], x[j]);
     }
 
     // ---- b = A conj(S)/|S| (arg(0) = 0); optional phase write
@@ -152,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tile_kernel(const TileArgs a)
             const bool in = (r < a.side) && (c < a.side);
             const int64_t gidx = (int64_t)r * a.side + c;
             const float A = in ? __ldg(a.amp_img + gidx) : 0.f;
-            const float x = sr[i][j], y = si[i][j];
+            const float x = f2_lo(sacc[i][j]), y = f2_hi(sacc[i][j]);
             hs_bvec_exact(x, y, A, br[i][j], bi[i][j]);
             if (WRITE && in) {
                 const int32_t di = __ldg(a.idx_img + gidx);
@@ -179,58 +208,35 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tile_kernel(const TileArgs a)
 
     // ---- forward: thread (rg, sg) holds rows 2 rg, 2 rg + 1 x spots sg + 8 j
     const int rg = tid >> 3, sg = tid & 7;
-    float tr0[SPT], ti0[SPT], tr1[SPT], ti1[SPT];
+    f2x t0[SPT], t1[SPT];
 #pragma unroll
-    for (int j = 0; j < SPT; ++j) tr0[j] = ti0[j] = tr1[j] = ti1[j] = 0.f;
+    for (int j = 0; j < SPT; ++j) t0[j] = t1[j] = 0ull;
 #pragma unroll 2
     for (int c = 0; c < kTileC; ++c) {
         const float4 b = *reinterpret_cast<const float4 *>(Bs + c * kBS + 2 * rg);
-        float2 x[SPT];
+        f2x x[SPT];
 #pragma unroll
-        for (int j = 0; j < SPT; ++j) x[j] = Xs[(sg + 8 * j) * kXS + c];
+        for (int j = 0; j < SPT; ++j) x[j] = X2[(sg + 8 * j) * kXS + c];
 #pragma unroll
-        for (int j = 0; j < SPT; ++j) {
-            tr0[j] = fmaf(b.x, x[j].x, tr0[j]);
-            ti0[j] = fmaf(b.x, x[j].y, ti0[j]);
-        }
+        for (int j = 0; j < SPT; ++j) f2_cmac(t0[j], b.x, b.y, x[j]);
 #pragma unroll
-        for (int j = 0; j < SPT; ++j) {
-            tr0[j] = fmaf(-b.y, x[j].y, tr0[j]);
-            ti0[j] = fmaf(b.y, x[j].x, ti0[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < SPT; ++j) {
-            tr1[j] = fmaf(b.z, x[j].x, tr1[j]);
-            ti1[j] = fmaf(b.z, x[j].y, ti1[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < SPT; ++j) {
-            tr1[j] = fmaf(-b.w, x[j].y, tr1[j]);
-            ti1[j] = fmaf(b.w, x[j].x, ti1[j]);
-        }
+        for (int j = 0; j < SPT; ++j) f2_cmac(t1[j], b.z, b.w, x[j]);
     }
     // E_k = sum_i gy[r][k] T[i][k] over the thread's two rows
     const int ra = min(r0 + 2 * rg, a.side - 1), rb = min(r0 + 2 * rg + 1, a.side - 1);
-    float er[SPT], ei[SPT];
+    f2x e2[SPT];
 #pragma unroll
     for (int j = 0; j < SPT; ++j) {
         const int k = sg + 8 * j;
         const float2 qa = __ldg(gy + (int64_t)ra * a.np + k);
         const float2 qb = __ldg(gy + (int64_t)rb * a.np + k);
-        float x = qa.x * tr0[j];
-        x = fmaf(-qa.y, ti0[j], x);
-        x = fmaf(qb.x, tr1[j], x);
-        x = fmaf(-qb.y, ti1[j], x);
-        float y = qa.x * ti0[j];
-        y = fmaf(qa.y, tr0[j], y);
-        y = fmaf(qb.x, ti1[j], y);
-        y = fmaf(qb.y, tr1[j], y);
-        er[j] = x;
-        ei[j] = y;
+        e2[j] = 0ull;
+        f2_cmac(e2[j], qa.x, qa.y, t0[j]);
+        f2_cmac(e2[j], qb.x, qb.y, t1[j]);
     }
     __syncthreads();  // b no longer read: its space becomes the row-group partials
 #pragma unroll
-    for (int j = 0; j < SPT; ++j) Rs[rg * KP + sg + 8 * j] = make_float2(er[j], ei[j]);
+    for (int j = 0; j < SPT; ++j) reinterpret_cast<f2x *>(Rs)[rg * KP + sg + 8 * j] = e2[j];
     __syncthreads();
     float2 *out = a.f.partials + (int64_t)pat * a.f.part_stride + (int64_t)tile * a.np;
     for (int k = tid; k < a.np; k += kThreads) {
