@@ -274,15 +274,14 @@ __global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs
     __syncwarp();
     stage(__ldg(a.chunk_c0 + q0));
     int rcur = -1;
-    float2 yn[NS];  // gy row of the stream's next run, loaded ahead of use
-    int yn_row = -1;
-    constexpr int DP = 2;  // lookahead in pairs
+    // smem address of this stream's entries in chunk buffer 0 / 1
+    const uint32_t ent0 = ent_a + 8u * (stream * P), ent1 = ent0 + 8u * kSlabL;
     int4 en = ent_pair(0, 0);
-    // pixel roles: lanes g < 8 finish pixel t ("mine") and send t+1's partial,
-    // lanes g >= 8 the reverse -- so the transpose-reduce needs no selects
 
     // One pair-trip = two pixels per 16-lane group (entries t, t+1 of a run;
-    // runs are padded to even length, so both share the row).
+    // runs are padded to even length, so both share the row).  The gy row of
+    // a new run is loaded when the run starts: 16 warps per SM hide the L2
+    // latency of the few row changes (one per ~3 pair-trips per warp).
     auto pair = [&](int qi, int t) {
         const int4 e = en;
         const int rc_m = lo ? e.x : e.z, rc_o = lo ? e.z : e.x;
@@ -290,29 +289,19 @@ __global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs
         f2x xm[NS], xo[NS];
         load_x(rc_m, xm);
         load_x(rc_o, xo);
-        {
-            const int tn = t + 2, qn = qi + (tn >= P);
-            if (qn < nq) en = ent_pair(qn, tn - (tn >= P ? P : 0));
-            const int tp = t + 2 * DP, qp = qi + (tp >= P);
-            if (qp < nq && yn_row < 0) {
-                const int rp = ent_pair(qp, tp - (tp >= P ? P : 0)).x >> 16;
-                if (rp != (e.x >> 16)) {
-                    load_y(rp, yn);
-                    yn_row = rp;
-                }
-            }
+        {   // next pair's entries (the next chunk's buffer after the last pair;
+            // past the CTA's last chunk the read is stale and unused)
+            const uint32_t nxt = (t + 2 < P) ? ((qi & 1) ? ent1 : ent0) + 8u * (t + 2) : ((qi & 1) ? ent0 : ent1);
+            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(en.x), "=r"(en.y), "=r"(en.z), "=r"(en.w)
+                         : "r"(nxt));
         }
         const int r = e.x >> 16;
         if (r != rcur) {  // warp-uniform: the 2 runs of a duo change row together
             if (rcur >= 0) flush();
-            if (r == yn_row) {
-                set_row(yn);
-                yn_row = -1;
-            } else {
-                float2 yq[NS];
-                load_y(r, yq);
-                set_row(yq);
-            }
+            float2 yq[NS];
+            load_y(r, yq);
+            set_row(yq);
             rcur = r;
         }
         // backward partials of both pixels over this lane's spots (FFMA2)
