@@ -29,15 +29,15 @@ __device__ __forceinline__ f2x f2_pack(float lo, float hi)
 
 __device__ __forceinline__ float f2_lo(f2x v)
 {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    float lo;
+    asm("{ .reg .f32 t;\n mov.b64 {%0, t}, %1; }" : "=f"(lo) : "l"(v));
     return lo;
 }
 
 __device__ __forceinline__ float f2_hi(f2x v)
 {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    float hi;
+    asm("{ .reg .f32 t;\n mov.b64 {t, %0}, %1; }" : "=f"(hi) : "l"(v));
     return hi;
 }
 

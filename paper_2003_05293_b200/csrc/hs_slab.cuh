@@ -3,28 +3,34 @@
 //
 // A window is a random 1/16 of the aperture (a storage-order range of the
 // seeded permutation, optics.py:184-187), so the gx row a pixel needs is a
-// random row of the pattern's table.  Gathering those rows from L2 made the
+// random row of the pattern's table.  Gathering those rows from L2 left the
 // window pass latency-bound (hs_win.cuh).  Here the grid is cut into column
 // slabs of `sw` columns whose gx rows fit in shared memory (sw * np * 8 B,
-// ~200 KB); the window list is ordered (slab, row, col) and cut into chunks
-// of 32 streams x P entries that never cross a slab.  A CTA
+// ~180 KB); the window list is ordered (slab, row-run) and cut into chunks of
+// 32 streams x kSlabP entries that never cross a slab.  A CTA
 //
-//   * stages its slab's gx rows with one TMA bulk copy (cp.async.bulk, an
-//     mbarrier with the byte count) -- re-staged only when its next chunk
+//   * stages its slab's gx rows with TMA bulk copies (cp.async.bulk onto an
+//     mbarrier carrying the byte count) -- re-staged only when its next chunk
 //     lies in another slab;
-//   * runs 32 independent pixel streams, 8 lanes per pixel, lane g owning
-//     spots {2(g+8j), 2(g+8j)+1}: each pixel reads its gx row from shared
-//     memory as float4 (one 128-B wavefront per 8-lane group, conflict-free);
-//   * keeps V = coef * gy[row] and T = sum_p b_p gx[c_p] per row in
-//     registers (the row-run scheme of hs_pass_kernel), E in registers;
-//   * prefetches the gy row of the entry three ahead into L1 and loads the
-//     entry stream five ahead, so row changes do not stall on L2.
+//   * runs 32 pixel streams: G lanes per pixel (G = 8: 4 streams per warp,
+//     8 warps; G = 16: 2 per warp, 16 warps), lane g owning spots
+//     VEC (g + G j) + h (VEC = 16 / G complex per shared load, so every group
+//     load is one conflict-free 128-B wavefront);
+//   * takes two pixels of a row-run per trip: their backward partials are
+//     finished by a transpose-reduce (half the group finishes each pixel),
+//     b = A conj(S)/|S| is exchanged by one shuffle, and both feed the
+//     forward accumulators T = sum_p b_p gx[c_p] of the run;
+//   * keeps V = coef gy[row] and T per run in registers (the streams of a
+//     warp change row on the same trip: runs are sorted by length and
+//     grouped per warp), flushing E += gy[row] T into per-stream shared
+//     memory at run ends.
 //
-// Per pixel-spot pair: one 8-B shared-memory read + 8 FFMA (backward
-// kernels.py:99-119, forward kernels.py:122-144).  Each chunk's partial is the
-// 8 warps' E summed in warp order; chunks are folded by hs_fold -- the
-// reduction shape depends only on the list, so results are bitwise
-// independent of the batch size and of how many chunks a CTA streams.
+// Complex MACs are FFMA2 (hs_f2.cuh).  Per pixel-spot pair: one 8-B shared
+// read + two complex MACs (backward kernels.py:99-119, forward
+// kernels.py:122-144).  A chunk's partial is its 32 streams' E summed in a
+// fixed order; chunks are folded by hs_fold -- the reduction shape depends
+// only on the list, so results are bitwise independent of the batch size
+// and of how many chunks a CTA streams.
 #pragma once
 
 #include "hs_f2.cuh"
@@ -32,10 +38,11 @@
 
 namespace hs {
 
-constexpr int kSlabThreads = 512;                // 16 warps
+constexpr int kSlabG = 16;                       // lanes per pixel (8 or 16)
+constexpr int kSlabThreads = 32 * kSlabG;        // 32 streams of kSlabG lanes
 constexpr int kSlabWarps = kSlabThreads / 32;
-constexpr int kSlabStreams = 32;                 // 16 warps x 2 pixel groups of 16 lanes
-constexpr int kSlabP = 16;                       // entries per stream per chunk
+constexpr int kSlabStreams = 32;                 // pixel streams per CTA
+constexpr int kSlabP = 32;                       // entries per stream per chunk
 constexpr int kSlabL = kSlabStreams * kSlabP;    // entries per chunk
 constexpr int kSlabSmemBudget = 220 * 1024;      // dynamic smem cap per CTA
 constexpr int kBulkPiece = 32 * 1024;            // bytes per cp.async.bulk
@@ -135,11 +142,16 @@ __device__ __forceinline__ void hs_sts2(uint32_t addr, float2 v)
     asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
 }
 
-template <int NS>
-__global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs a)
+template <int NS, int G>
+__global__ void __launch_bounds__(32 * G, 1) hs_slab_kernel(const SlabArgs a)
 {
+    constexpr int NT = 32 * G;          // threads
+    constexpr int GPW = 32 / G;         // pixel groups (streams) per warp
+    constexpr int VEC = 16 / G;         // complex values per lane per shared load
     constexpr int NP = 16 * NS;
+    constexpr int SPL = VEC * NS;       // spots per lane
     constexpr int P = kSlabP;
+    static_assert(GPW * (NT / 32) == kSlabStreams, "32 streams per CTA");
     extern __shared__ float4 sm4[];
     __shared__ __align__(8) unsigned long long bar;
 
@@ -149,31 +161,37 @@ __global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs
     const int nq = min(a.cpc, a.f.chunk_end - q0);
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
-    const int g = lane & 15, s = lane >> 4;
-    const bool lo = g < 8;
-    const int stream = warp * 2 + s;
+    const int g = lane & (G - 1), s = lane / G;
+    const bool lo = g < G / 2;
+    const int stream = warp * GPW + s;
 
     float2 *Xs = reinterpret_cast<float2 *>(sm4);                 // [sw][NP]
     float2 *Es = Xs + (size_t)a.sw * NP;                            // [32][NP]
     int2 *Ent = reinterpret_cast<int2 *>(Es + kSlabStreams * NP);   // [2][kSlabL]
     float2 *coef_s = reinterpret_cast<float2 *>(Ent + 2 * kSlabL);  // [NP]
-    const uint32_t xs_a = hs_smem_addr(Xs) + 8u * g;
-    const uint32_t es_a = hs_smem_addr(Es) + 8u * (stream * NP + g);
+    // lane's first complex in a table row: spot VEC g (stride VEC G per j)
+    const uint32_t xs_a = hs_smem_addr(Xs) + 8u * VEC * g;
+    const uint32_t es_a = hs_smem_addr(Es) + 8u * (stream * NP + VEC * g);
     const uint32_t ent_a = hs_smem_addr(Ent);
-    const uint32_t cf_a = hs_smem_addr(coef_s) + 8u * g;
+    const uint32_t cf_a = hs_smem_addr(coef_s) + 8u * VEC * g;
 
-    for (int k = tid; k < NP; k += kSlabThreads) coef_s[k] = a.coef[(int64_t)pat * NP + k];
-    for (int k = tid; k < kSlabStreams * NP; k += kSlabThreads) Es[k] = make_float2(0.f, 0.f);
+    for (int k = tid; k < NP; k += NT) coef_s[k] = a.coef[(int64_t)pat * NP + k];
+    for (int k = tid; k < kSlabStreams * NP; k += NT) Es[k] = make_float2(0.f, 0.f);
 
-    // per-warp entry staging: the warp's 2 streams of chunk q are the 2P
-    // entries [2 w P, 2 (w+1) P) of the chunk -- one int2 per lane
-    static_assert(2 * kSlabP == 32, "one entry per lane per warp segment");
-    int2 ent_reg = make_int2(0, 0);
+    // per-warp entry staging: the warp's GPW streams of chunk q are the
+    // GPW * P entries [w GPW P, (w+1) GPW P) of the chunk
+    constexpr int EPL = GPW * P / 32;  // entries per lane
+    int2 ent_reg[EPL];
     auto fetch_ent = [&](int qi) {
-        if (qi < nq) ent_reg = __ldg(a.ent + (int64_t)(q0 + qi) * kSlabL + warp * 2 * P + lane);
+        if (qi < nq)
+#pragma unroll
+            for (int k = 0; k < EPL; ++k)
+                ent_reg[k] = __ldg(a.ent + (int64_t)(q0 + qi) * kSlabL + warp * GPW * P + lane + 32 * k);
     };
     auto store_ent = [&](int qi) {
-        if (qi < nq) Ent[(qi & 1) * kSlabL + warp * 2 * P + lane] = ent_reg;
+        if (qi < nq)
+#pragma unroll
+            for (int k = 0; k < EPL; ++k) Ent[(qi & 1) * kSlabL + warp * GPW * P + lane + 32 * k] = ent_reg[k];
     };
     fetch_ent(0);
     store_ent(0);
@@ -187,7 +205,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs
     __syncthreads();
 
     const float2 *__restrict__ gx = a.gx + (int64_t)pat * a.tab_stride;
-    const float2 *__restrict__ Y = a.gy + (int64_t)pat * a.tab_stride + g;
+    const float2 *__restrict__ Y = a.gy + (int64_t)pat * a.tab_stride + VEC * g;
     uint32_t phase = 0;
     int c0 = -1;
 
@@ -223,52 +241,62 @@ __global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs
         c0 = cs;
     };
 
-    // lane state: spots g + 16 j, j < NS; complex values packed (re, im)
-    float vr[NS], vi[NS], yr_[NS], yi_[NS];
-    f2x tt[NS];
+    // lane state (SPL spots): V = coef * gy[row], gy[row], T packed (re, im)
+    float vr[SPL], vi[SPL], yr_[SPL], yi_[SPL];
+    f2x tt[SPL];
 #pragma unroll
-    for (int k = 0; k < NS; ++k) {
+    for (int k = 0; k < SPL; ++k) {
         vr[k] = vi[k] = yr_[k] = yi_[k] = 0.f;
         tt[k] = 0ull;
     }
 
-    auto ent_pair = [&](int qi, int t) -> int4 {  // entries t, t+1 (t even) of this stream
-        int4 v;
-        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                     : "r"(ent_a + 8u * ((qi & 1) * kSlabL + stream * P + t)));
-        return v;
+    // shared loads of VEC complex values (one lane's slice of a row)
+    auto lds_vec = [&](uint32_t addr, f2x *d) {
+        if constexpr (VEC == 2)
+            asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(d[0]), "=l"(d[VEC - 1]) : "r"(addr));
+        else
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(d[0]) : "r"(addr));
     };
-    auto load_x = [&](int rc, f2x (&x)[NS]) {
+    auto sts_vec = [&](uint32_t addr, const f2x *d) {
+        if constexpr (VEC == 2)
+            asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(addr), "l"(d[0]), "l"(d[VEC - 1]) : "memory");
+        else
+            asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"(d[0]) : "memory");
+    };
+    auto load_x = [&](int rc, f2x (&x)[SPL]) {
         const uint32_t row = xs_a + 8u * NP * (uint32_t)(rc & 0xffff);  // slab-local column
 #pragma unroll
-        for (int j = 0; j < NS; ++j) asm volatile("ld.shared.b64 %0, [%1];" : "=l"(x[j]) : "r"(row + 128u * j));
+        for (int j = 0; j < NS; ++j) lds_vec(row + 8u * VEC * G * j, &x[VEC * j]);
     };
     auto flush = [&]() {  // Es[stream] += Y * T ; T = 0
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
-            f2x e;
-            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(e) : "r"(es_a + 128u * j));
-            f2_cmac(e, yr_[j], yi_[j], tt[j]);
-            tt[j] = 0ull;
-            asm volatile("st.shared.b64 [%0], %1;" ::"r"(es_a + 128u * j), "l"(e) : "memory");
-        }
-    };
-    auto set_row = [&](const float2 (&yq)[NS]) {  // Y = row, V = coef * Y
+            f2x e[VEC];
+            lds_vec(es_a + 8u * VEC * G * j, e);
 #pragma unroll
-        for (int j = 0; j < NS; ++j) {
-            const float2 q = yq[j];
-            const float2 w = hs_lds2(cf_a + 128u * j);
-            yr_[j] = q.x;
-            yi_[j] = q.y;
-            vr[j] = fmaf(w.x, q.x, -w.y * q.y);
-            vi[j] = fmaf(w.x, q.y, w.y * q.x);
+            for (int h = 0; h < VEC; ++h) {
+                const int k = VEC * j + h;
+                f2_cmac(e[h], yr_[k], yi_[k], tt[k]);
+                tt[k] = 0ull;
+            }
+            sts_vec(es_a + 8u * VEC * G * j, e);
         }
     };
-    auto load_y = [&](int r, float2 (&yq)[NS]) {
+    auto new_row = [&](int r) {  // Y = gy[r], V = coef * Y
         const float2 *yrow = Y + (int64_t)r * NP;
 #pragma unroll
-        for (int j = 0; j < NS; ++j) yq[j] = __ldg(yrow + 16 * j);
+        for (int j = 0; j < NS; ++j) {
+#pragma unroll
+            for (int h = 0; h < VEC; ++h) {
+                const int k = VEC * j + h;
+                const float2 q = __ldg(yrow + VEC * G * j + h);
+                const float2 w = hs_lds2(cf_a + 8u * (VEC * G * j + h));
+                yr_[k] = q.x;
+                yi_[k] = q.y;
+                vr[k] = fmaf(w.x, q.x, -w.y * q.y);
+                vi[k] = fmaf(w.x, q.y, w.y * q.x);
+            }
+        }
     };
 
     __syncwarp();
@@ -276,17 +304,18 @@ __global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs
     int rcur = -1;
     // smem address of this stream's entries in chunk buffer 0 / 1
     const uint32_t ent0 = ent_a + 8u * (stream * P), ent1 = ent0 + 8u * kSlabL;
-    int4 en = ent_pair(0, 0);
+    int4 en;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(en.x), "=r"(en.y), "=r"(en.z), "=r"(en.w) : "r"(ent0));
 
-    // One pair-trip = two pixels per 16-lane group (entries t, t+1 of a run;
-    // runs are padded to even length, so both share the row).  The gy row of
-    // a new run is loaded when the run starts: 16 warps per SM hide the L2
-    // latency of the few row changes (one per ~3 pair-trips per warp).
+    // One pair-trip = two pixels per group (entries t, t+1 of a run; runs are
+    // padded to even length, so both share the row).  Lanes g < G/2 finish
+    // pixel t ("mine") and hand t+1's partial over, lanes g >= G/2 the
+    // reverse, so the transpose-reduce needs no selects.
     auto pair = [&](int qi, int t) {
         const int4 e = en;
         const int rc_m = lo ? e.x : e.z, rc_o = lo ? e.z : e.x;
         const float A_m = __int_as_float(lo ? e.y : e.w);
-        f2x xm[NS], xo[NS];
+        f2x xm[SPL], xo[SPL];
         load_x(rc_m, xm);
         load_x(rc_o, xo);
         {   // next pair's entries (the next chunk's buffer after the last pair;
@@ -297,73 +326,82 @@ __global__ void __launch_bounds__(kSlabThreads, 1) hs_slab_kernel(const SlabArgs
                          : "r"(nxt));
         }
         const int r = e.x >> 16;
-        if (r != rcur) {  // warp-uniform: the 2 runs of a duo change row together
+        if (r != rcur) {  // warp-uniform: a warp's runs change row together
             if (rcur >= 0) flush();
-            float2 yq[NS];
-            load_y(r, yq);
-            set_row(yq);
+            new_row(r);
             rcur = r;
         }
         // backward partials of both pixels over this lane's spots (FFMA2)
         f2x m0 = 0ull, m1 = 0ull, o0 = 0ull, o1 = 0ull;
 #pragma unroll
-        for (int k = 0; k < NS; ++k) {
+        for (int k = 0; k < SPL; ++k) {
             f2_cmac((k & 1) ? m1 : m0, vr[k], vi[k], xm[k]);
             f2_cmac((k & 1) ? o1 : o0, vr[k], vi[k], xo[k]);
         }
         float kr = f2_lo(m0) + f2_lo(m1), ki = f2_hi(m0) + f2_hi(m1);
         const float sr_o = f2_lo(o0) + f2_lo(o1), si_o = f2_hi(o0) + f2_hi(o1);
-        // transpose-reduce over the 16 lanes (commutative butterflies: every
+        // transpose-reduce over the G lanes (commutative butterflies: every
         // lane of a half ends with identical bits)
-        kr += __shfl_xor_sync(0xffffffffu, sr_o, 8);
-        ki += __shfl_xor_sync(0xffffffffu, si_o, 8);
+        kr += __shfl_xor_sync(0xffffffffu, sr_o, G / 2);
+        ki += __shfl_xor_sync(0xffffffffu, si_o, G / 2);
 #pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
+        for (int o = G / 4; o > 0; o >>= 1) {
             kr += __shfl_xor_sync(0xffffffffu, kr, o);
             ki += __shfl_xor_sync(0xffffffffu, ki, o);
         }
         float mr, mi;
         hs_bvec(kr, ki, A_m, mr, mi);
-        const float orr = __shfl_xor_sync(0xffffffffu, mr, 8);
-        const float oi = __shfl_xor_sync(0xffffffffu, mi, 8);
+        const float orr = __shfl_xor_sync(0xffffffffu, mr, G / 2);
+        const float oi = __shfl_xor_sync(0xffffffffu, mi, G / 2);
 #pragma unroll
-        for (int k = 0; k < NS; ++k) f2_cmac(tt[k], mr, mi, xm[k]);
+        for (int k = 0; k < SPL; ++k) f2_cmac(tt[k], mr, mi, xm[k]);
 #pragma unroll
-        for (int k = 0; k < NS; ++k) f2_cmac(tt[k], orr, oi, xo[k]);
+        for (int k = 0; k < SPL; ++k) f2_cmac(tt[k], orr, oi, xo[k]);
     };
 
-    // End of chunk qi: flush, sum the 32 streams in order, reset, stage.
+    // End of chunk qi: flush, sum the 32 streams in a fixed order, reset, stage.
     auto chunk_end = [&](int qi) {
         if (rcur >= 0) flush();
         rcur = -1;
-        __syncthreads();
         float2 *out = a.f.partials + (int64_t)pat * a.f.part_stride + (int64_t)(q0 + qi) * NP;
-        // streams 2w, 2w+1 of warp w: symmetric add by shuffle, kept in
-        // stream 2w's row; then the 16 warp rows summed in warp order
+        // the warp's GPW streams: symmetric butterfly adds, kept in stream
+        // GPW w's row; then the warp rows summed in warp order
         {
-            const uint32_t w0 = hs_smem_addr(Es) + 8u * (2 * warp * NP + g);
+            const uint32_t w0 = hs_smem_addr(Es) + 8u * (GPW * warp * NP + VEC * g);
 #pragma unroll
             for (int j = 0; j < NS; ++j) {
-                const float2 v = hs_lds2(es_a + 128u * j);
-                float2 o;
-                o.x = v.x + __shfl_xor_sync(0xffffffffu, v.x, 16);
-                o.y = v.y + __shfl_xor_sync(0xffffffffu, v.y, 16);
-                if (s == 0) hs_sts2(w0 + 128u * j, o);
-                else hs_sts2(es_a + 128u * j, make_float2(0.f, 0.f));
+                f2x v[VEC];
+                lds_vec(es_a + 8u * VEC * G * j, v);
+#pragma unroll
+                for (int h = 0; h < VEC; ++h) {
+                    float x = f2_lo(v[h]), y = f2_hi(v[h]);
+#pragma unroll
+                    for (int o = G; o < 32; o <<= 1) {
+                        x += __shfl_xor_sync(0xffffffffu, x, o);
+                        y += __shfl_xor_sync(0xffffffffu, y, o);
+                    }
+                    v[h] = f2_pack(x, y);
+                }
+                if (s == 0) {
+                    sts_vec(w0 + 8u * VEC * G * j, v);
+                } else {
+                    const f2x z[VEC == 2 ? 2 : 1] = {};
+                    sts_vec(es_a + 8u * VEC * G * j, z);
+                }
             }
         }
         __syncthreads();
-        for (int k = tid; k < NP; k += kSlabThreads) {
+        for (int k = tid; k < NP; k += NT) {
             float x = 0.f, y = 0.f;
 #pragma unroll
-            for (int w = 0; w < kSlabWarps; ++w) {
-                const float2 v = Es[2 * w * NP + k];
+            for (int w = 0; w < NT / 32; ++w) {
+                const float2 v = Es[GPW * w * NP + k];
                 x += v.x;
                 y += v.y;
             }
             out[k] = make_float2(x, y);
 #pragma unroll
-            for (int w = 0; w < kSlabWarps; ++w) Es[2 * w * NP + k] = make_float2(0.f, 0.f);
+            for (int w = 0; w < NT / 32; ++w) Es[GPW * w * NP + k] = make_float2(0.f, 0.f);
         }
         store_ent(qi + 2);  // chunk qi's buffer is consumed
         __syncwarp();
