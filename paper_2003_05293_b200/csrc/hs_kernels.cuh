@@ -86,7 +86,6 @@ struct PassArgs {
     int32_t chunk_len;        // entries per CTA; multiple of 8 * SPW
     int32_t np, nl;           // padded spot count, spots per lane (even)
     int32_t sorted_rows;      // list is sorted by row (window lists)
-    int32_t cpc;              // logical chunks per CTA (divides kGroup; window kernel)
     int64_t tab_stride;       // side * np
     const float2 *gx, *gy;    // [B][side][np]
     const float2 *coef;       // [B][np]

@@ -24,7 +24,6 @@
 #include "hs_kernels.cuh"
 #include "hs_tile.cuh"
 #include "hs_slab.cuh"
-#include "hs_win.cuh"
 
 using namespace hs;
 
@@ -149,7 +148,6 @@ struct hs_plan {
     int32_t *d_idx_img = nullptr;         // [side][side] storage index, -1 outside
     int32_t *d_tiles = nullptr;           // non-empty 64x32 tiles, packed (r0 << 16) | c0
     int32_t ntiles = 0;
-    int win_minb = 2;                     // resident CTAs/SM the window kernel is built for
     int num_sms = 148;
     DevList storage;                      // storage order
     std::map<int, DevList> dense;         // full range, banded layout per slots-per-warp
@@ -690,18 +688,8 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
     if (l.sw > 0) return launch_slab(p, mode, l, geo.nchunks, u, lo, hi);
     a.f = fold_args(p, geo.nchunks, u, lo, hi);
     dim3 grid(hi - lo, p->batch);
-    if (l.sorted_rows && c.ns > 0 && mode == (PM_BWD | PM_FWD)) {
-        // compressed window: latency-shaped kernel (16 lanes per pixel); a
-        // CTA streams cpc logical chunks when the batch gives enough CTAs
-        int cpc = 1;
-        while (cpc < kMaxCpc && (int64_t)geo.nchunks * p->batch / (2 * cpc) >= 4 * kTargetChunks) cpc *= 2;
-        a.cpc = cpc;
-        grid.x = (hi - lo + cpc - 1) / cpc;
-        hs_select_win(c.ns, p->win_minb)<<<grid, kThreads, hs_win_smem_bytes(c.ns), p->stream>>>(a);
-    } else {
-        PassFn fn = select_pass(c, mode);
-        fn<<<grid, kThreads, pass_smem(c), p->stream>>>(a);
-    }
+    PassFn fn = select_pass(c, mode);
+    fn<<<grid, kThreads, pass_smem(c), p->stream>>>(a);
     CUDA_TRY(cudaGetLastError());
     return HS_OK;
 }
@@ -874,16 +862,11 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
         CUDA_TRY(cudaMemcpy(p->d_amp_img, amp_img.data(), cells * sizeof(float), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(p->d_idx_img, p->h_index.data(), cells * sizeof(int32_t), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-        if (const char *env = getenv("HS_WIN_MINB")) p->win_minb = atoi(env);
         CUDA_TRY(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
         for (int ns = 1; ns <= 8; ++ns)
             CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_slab(ns),
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           kSlabSmemBudget));  // process-wide cap: never lower it per plan
-        for (int ns = 1; ns <= 8; ++ns)
-            for (int mb = 2; mb <= 4; ++mb)
-                CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_win(ns, mb),
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs_win_smem_bytes(ns)));
         for (int spt = 1; spt <= 16; ++spt)
             for (int w = 0; w < 2; ++w)
                 CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_tile(spt, w != 0),
