@@ -41,8 +41,10 @@ SIDE, NSPOTS, COMPRESSION, ITERS = 1152, 100, 1 / 16, 20
 FLOP_PER_PAIR_PASS = 8  # one complex MAC per (pixel, spot) per pass
 
 
-def workload_config(batch):
+def workload_config(batch, world=1):
     return {"workload": "cswgs_1152_n100_c1/16_i20_batched", "side_px": SIDE,
+            "parallelism": f"batch-dp{world} (independent patterns per rank, no data-path "
+                           "collective)",
             "spots": NSPOTS, "compression": COMPRESSION, "iterations": ITERS,
             "batch_per_gpu": batch, "pupil": "gaussian waist 6 mm, pitch 9.2 um, "
             "lambda 800 nm, f 20 mm, seed 0", "foci": "uniform xy +-100 um, z +-50 um, "
@@ -109,12 +111,21 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def host_threads():
+    """All host cores this process may run on (torchrun pins OMP_NUM_THREADS=1,
+    the oracle's OpenMP regions take an explicit thread count instead)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def cpu_oracle_rate(seconds=10.0, threads=None):
     """Oracle (bit-exact reference restatement) holograms/s on host cores."""
     import oracle
     import paper_2003_05293_b200 as hs
     pupil = hs.build_pupil(SIDE)
-    threads = threads or oracle.max_threads()
+    threads = threads or host_threads()
     done, t0 = 0, time.perf_counter()
     while True:
         s = hs.random_foci(NSPOTS, 1000 + done)
@@ -136,7 +147,7 @@ def run_reference(args):
     import paper_2003_05293_b200 as hs
     oracle.build()
     pupil = hs.build_pupil(SIDE)
-    threads = oracle.max_threads()
+    threads = host_threads()
 
     def step(k):
         s = hs.random_foci(NSPOTS, 1000 + k)
@@ -154,7 +165,7 @@ def run_reference(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(1),
+            "config": workload_config(1, world),
             "cpu_baseline": {"value": val, "unit": "holograms/s", "cores": threads,
                              "kind": "port", "sample": f"{args.steps} holograms of the "
                              "workload, 1 per step (C+OpenMP oracle, bit-exact vs reference)"},
@@ -171,13 +182,21 @@ def run_ours(args):
     from paper_2003_05293_b200 import _lib
 
     rank, local, world = dist_env()
+    ndev = torch.cuda.device_count()
+    # one process per GPU; ranks beyond the visible GPUs (a multi-rank smoke
+    # run on a 1-GPU box) share devices and time through gloo instead of NCCL
+    shared = world > ndev
+    local = local % ndev
+    torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         dist = None
-        torch.cuda.set_device(local)
+    coll_dev = "cpu" if shared else f"cuda:{local}"
     _lib.set_device(local)
     B = args.batch
     pupil = hs.build_pupil(SIDE)
@@ -218,7 +237,7 @@ def run_ours(args):
     if np.any(status != 0):
         raise RuntimeError(f"solver failed on patterns {np.nonzero(status)[0]}")
     if dist is not None:
-        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        t = torch.tensor([total_ms], device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     value = world * B * args.steps / (total_ms * 1e-3)
@@ -275,7 +294,7 @@ def run_ours(args):
     e2e_plan.sync()
     e2e_s = time.perf_counter() - t0
     if dist is not None:
-        t = torch.tensor([e2e_s], device=f"cuda:{local}")
+        t = torch.tensor([e2e_s], device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = world * B * e2e_steps / e2e_s
@@ -315,7 +334,7 @@ def run_ours(args):
         "ms_per_hologram": total_ms / args.steps / B,
         "latency_ms_single_hologram": latency_ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
-        "data": "synthetic", "config": workload_config(B),
+        "data": "synthetic", "config": workload_config(B, world),
         "e2e": {"value": e2e_value, "unit": "holograms/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps, "matches_device_e": e2e_ok,
                 "path": "hs_solve_host_async (C ABI, pinned host buffers, phase f64 storage "
