@@ -20,7 +20,12 @@ from .optics import (CompressionPlan, Hologram, Pupil, SpotSet, build_pupil, pha
 from .solvers import (PlannedRun, SolverConfig, SolverTrace, StepRecord, WgsState,
                       budget_controller, cswgs, predict_ops, rebalance_weights, rs, solve,
                       solve_batch, wgs, wgs_step)
+from .scenarios import (SCENARIO_NAMES, Scenario, cubes_scenario, grid_scenario,
+                        load_scenario_file, named_scenario, rotate_points, rotation_sweep)
+from .sequences import rotation_sequence, sequence_quality, solve_sequence
 from .simulate import FieldImage, probe_intensities, render_plane
+from .sweeps import (BenchRecord, BudgetComparison, CellStats, calibrate_ops_per_ms,
+                     compare_at_budget, frame_budget_ops, summarize, sweep)
 from .slm import PhaseLut, slm_raster, solve_rasters
 from ._lib import get_device, set_device
 from .workloads import grid_spots, named_spots, random_foci

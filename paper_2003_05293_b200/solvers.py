@@ -148,11 +148,15 @@ class BatchResult:
 
 
 def _run_batch(algorithm: str, pupil: Pupil, spot_sets, iterations: int, subset: int,
-               seeds, fetch_phase: bool = True, raster: bool = False) -> BatchResult:
+               seeds, fetch_phase: bool = True, raster: bool = False,
+               theta0: np.ndarray | None = None) -> BatchResult:
     plan = _lib.plan_for(pupil)
     plan.set_spots(spot_sets)
     n = plan.n
-    theta0 = np.stack([_theta0(int(s), n) for s in seeds])
+    if theta0 is None:
+        theta0 = np.stack([_theta0(int(s), n) for s in seeds])
+    else:
+        theta0 = np.ascontiguousarray(theta0, dtype=np.float64).reshape(len(spot_sets), n)
     iters = 0 if algorithm == "rs" else iterations
     plan.solve(_ALG_CODE[algorithm], iters, subset, theta0, want_fields=True, raster=raster)
     status, deg = plan.status()
