@@ -149,6 +149,7 @@ struct hs_plan {
     int32_t *d_tiles = nullptr;           // non-empty 64x32 tiles, packed (r0 << 16) | c0
     int32_t ntiles = 0;
     int num_sms = 148;
+    size_t l2_window = 0;                 // bytes of gx|gy marked L2-persisting
     DevList storage;                      // storage order
     std::map<int, DevList> dense;         // full range, banded layout per slots-per-warp
     // compressed windows keyed (start, count, np): slab-ordered for np <= 128
@@ -454,7 +455,7 @@ void free_batch(hs_plan *p)
 {
     dfree(p->d_x); dfree(p->d_y); dfree(p->d_z); dfree(p->d_a0);
     dfree(p->d_theta); dfree(p->d_amp_in);
-    dfree(p->d_gx); dfree(p->d_gy); dfree(p->d_w); dfree(p->d_coef);
+    dfree(p->d_gx); p->d_gy = nullptr; dfree(p->d_w); dfree(p->d_coef);
     dfree(p->d_status); dfree(p->d_degen); dfree(p->d_qstatus);
     dfree(p->d_fields); dfree(p->d_e); dfree(p->d_u); dfree(p->d_inten); dfree(p->d_rel);
     dfree(p->d_out[1]);
@@ -468,6 +469,35 @@ void free_batch(hs_plan *p)
     free_graphs(p);
 }
 
+// The gx / gy tables are re-read by every pass (each window pass gathers
+// random rows of them); the pipelined host API streams the previous solve's
+// phases (267 MB at B = 32) device-to-host through L2 at the same time.  An
+// access-policy window on the solver stream (captured into the graphs'
+// kernel nodes) marks the tables persisting, so that traffic does not evict
+// them.  HS_L2_PERSIST=0 disables it.
+int set_l2_policy(hs_plan *p, size_t bytes)
+{
+    const char *env = getenv("HS_L2_PERSIST");
+    if (env && atoi(env) == 0) return HS_OK;
+    int maxp = 0, maxw = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, p->device));
+    CUDA_TRY(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, p->device));
+    if (maxp <= 0 || maxw <= 0) return HS_OK;
+    const size_t win = std::min(bytes, (size_t)maxw);
+    const size_t keep = std::min(win, (size_t)maxp);
+    CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, keep));
+    cudaStreamAttrValue v;
+    memset(&v, 0, sizeof v);
+    v.accessPolicyWindow.base_ptr = p->d_gx;
+    v.accessPolicyWindow.num_bytes = win;
+    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)keep / (double)win);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CUDA_TRY(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
+    p->l2_window = win;
+    return HS_OK;
+}
+
 int ensure_batch(hs_plan *p, int batch, int n)
 {
     const Config cfg = pick_config(n);
@@ -478,8 +508,7 @@ int ensure_batch(hs_plan *p, int batch, int n)
     int rc;
     if ((rc = dalloc(&p->d_x, bn)) || (rc = dalloc(&p->d_y, bn)) || (rc = dalloc(&p->d_z, bn)) ||
         (rc = dalloc(&p->d_a0, bn)) || (rc = dalloc(&p->d_theta, bn)) || (rc = dalloc(&p->d_amp_in, bn)) ||
-        (rc = dalloc(&p->d_gx, (size_t)B * p->side * cfg.np)) ||
-        (rc = dalloc(&p->d_gy, (size_t)B * p->side * cfg.np)) || (rc = dalloc(&p->d_w, bn)) ||
+        (rc = dalloc(&p->d_gx, (size_t)2 * B * p->side * cfg.np)) || (rc = dalloc(&p->d_w, bn)) ||
         (rc = dalloc(&p->d_coef, bn)) || (rc = dalloc(&p->d_status, B)) || (rc = dalloc(&p->d_degen, B)) ||
         (rc = dalloc(&p->d_qstatus, B)) || (rc = dalloc(&p->d_fields, bn * 2)) || (rc = dalloc(&p->d_e, B)) ||
         (rc = dalloc(&p->d_u, B)) || (rc = dalloc(&p->d_inten, bn)) || (rc = dalloc(&p->d_rel, bn)) ||
@@ -489,10 +518,11 @@ int ensure_batch(hs_plan *p, int batch, int n)
         return rc;
     }
     CUDA_TRY(cudaMemset(p->d_status, 0, sizeof(int32_t) * B));
+    p->d_gy = p->d_gx + (size_t)B * p->side * cfg.np;  // one allocation: gx | gy
     p->d_out[0] = p->d_phase;
     p->cap_batch = B;
     p->cap_np = cfg.np;
-    return HS_OK;
+    return set_l2_policy(p, (size_t)2 * B * p->side * cfg.np * sizeof(float2));
 }
 
 // Fold buffers sized for `chunks` partials per pattern.
