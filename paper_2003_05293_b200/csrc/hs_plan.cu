@@ -149,7 +149,6 @@ struct hs_plan {
     int32_t *d_tiles = nullptr;           // non-empty 64x32 tiles, packed (r0 << 16) | c0
     int32_t ntiles = 0;
     int num_sms = 148;
-    size_t l2_window = 0;                 // bytes of gx|gy marked L2-persisting
     DevList storage;                      // storage order
     std::map<int, DevList> dense;         // full range, banded layout per slots-per-warp
     // compressed windows keyed (start, count, np): slab-ordered for np <= 128
@@ -469,35 +468,6 @@ void free_batch(hs_plan *p)
     free_graphs(p);
 }
 
-// The gx / gy tables are re-read by every pass (each window pass gathers
-// random rows of them); the pipelined host API streams the previous solve's
-// phases (267 MB at B = 32) device-to-host through L2 at the same time.  An
-// access-policy window on the solver stream (captured into the graphs'
-// kernel nodes) marks the tables persisting, so that traffic does not evict
-// them.  HS_L2_PERSIST=0 disables it.
-int set_l2_policy(hs_plan *p, size_t bytes)
-{
-    const char *env = getenv("HS_L2_PERSIST");
-    if (env && atoi(env) == 0) return HS_OK;
-    int maxp = 0, maxw = 0;
-    CUDA_TRY(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, p->device));
-    CUDA_TRY(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, p->device));
-    if (maxp <= 0 || maxw <= 0) return HS_OK;
-    const size_t win = std::min(bytes, (size_t)maxw);
-    const size_t keep = std::min(win, (size_t)maxp);
-    CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, keep));
-    cudaStreamAttrValue v;
-    memset(&v, 0, sizeof v);
-    v.accessPolicyWindow.base_ptr = p->d_gx;
-    v.accessPolicyWindow.num_bytes = win;
-    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)keep / (double)win);
-    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    CUDA_TRY(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
-    p->l2_window = win;
-    return HS_OK;
-}
-
 int ensure_batch(hs_plan *p, int batch, int n)
 {
     const Config cfg = pick_config(n);
@@ -522,7 +492,7 @@ int ensure_batch(hs_plan *p, int batch, int n)
     p->d_out[0] = p->d_phase;
     p->cap_batch = B;
     p->cap_np = cfg.np;
-    return set_l2_policy(p, (size_t)2 * B * p->side * cfg.np * sizeof(float2));
+    return HS_OK;
 }
 
 // Fold buffers sized for `chunks` partials per pattern.
