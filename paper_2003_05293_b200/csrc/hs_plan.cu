@@ -23,6 +23,7 @@
 #include "../../include/holospots_b200.h"
 #include "hs_kernels.cuh"
 #include "hs_tile.cuh"
+#include "hs_tilek.cuh"
 #include "hs_slab.cuh"
 
 using namespace hs;
@@ -607,10 +608,13 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     a.f = fold_args(p, p->ntiles, u, lo, hi);
     a.n = p->n;
     const int spt = (p->n + 7) / 8;
-    TileFn fn = hs_select_tile(spt, write);
+    // n <= 128: all spots resident (hs_tile); larger n: spot-chunked (hs_tilek)
+    const bool chunked = c.ns == 0;
+    TileFn fn = chunked ? hs_select_tilek(write) : hs_select_tile(spt, write);
+    const size_t smem = chunked ? hs_tilek_smem_bytes() : hs_tile_smem_bytes(spt, p->n);
     if (hi <= lo) return HS_OK;
     dim3 grid(hi - lo, p->batch);
-    fn<<<grid, kThreads, hs_tile_smem_bytes(spt, p->n), p->stream>>>(a);
+    fn<<<grid, kThreads, smem, p->stream>>>(a);
     CUDA_TRY(cudaGetLastError());
     return HS_OK;
 }
@@ -727,7 +731,7 @@ int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags, doub
     if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
     const int final_mode = want_fields ? (PM_BWD | PM_FWD | PM_WRITE) : (PM_BWD | PM_WRITE);
     const UpdArgs fin = upd_args(p, want_fields ? ACT_FINAL : ACT_NONE);
-    const bool tiled = p->cfg.ns > 0;
+    const bool tiled = true;  // GEMM-tile full passes for every n (hs_tile / hs_tilek)
     unsigned char *raster = (flags & HS_WANT_RASTER) ? p->d_raster : nullptr;
     if (raster)
         CUDA_TRY(cudaMemsetAsync(raster, 0, (size_t)p->batch * p->side * p->side, p->stream));
@@ -867,6 +871,9 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
             CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_slab(ns),
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           kSlabSmemBudget));  // process-wide cap: never lower it per plan
+        for (int w = 0; w < 2; ++w)
+            CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_tilek(w != 0),
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs_tilek_smem_bytes()));
         for (int spt = 1; spt <= 16; ++spt)
             for (int w = 0; w < 2; ++w)
                 CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_tile(spt, w != 0),
@@ -1254,14 +1261,11 @@ static int shard_pass_desc(hs_plan *p, int j, int *kind, const DevList **list, i
         const int64_t off = (j == 0) ? 0 : ((int64_t)(j - 1) * sh.half) % (m - sh.subset + 1);
         if ((rc = get_window(p, off, sh.subset, &lst))) return rc;
         *kind = 1;
-    } else if (p->cfg.ns > 0) {
-        *kind = 0;
+    } else {
+        *kind = 0;  // GEMM-tile full pass (every n)
         *list = nullptr;
         *nchunks = p->ntiles;
         return HS_OK;
-    } else {
-        if ((rc = get_dense(p, p->cfg.spw, &lst))) return rc;
-        *kind = 1;
     }
     *list = lst;
     *nchunks = geom_of(*lst, lst->count, p->cfg.spw).nchunks;
@@ -1485,7 +1489,7 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
     CUDA_TRY(cudaEventCreate(&e1));
     const UpdArgs u = upd_args(p, ACT_FIELDS);
     auto once = [&]() -> int {
-        if (which == 0 && p->cfg.ns > 0) return launch_tile(p, false, u, nullptr);
+        if (which == 0) return launch_tile(p, false, u, nullptr);
         return launch_pass(p, PM_BWD | PM_FWD, *l, 0, l->count, 0, nullptr, nullptr, 0, u);
     };
     if ((rc = reset_status(p)) || (rc = once())) return rc;
