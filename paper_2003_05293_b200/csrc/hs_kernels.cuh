@@ -98,6 +98,22 @@ struct PassArgs {
 };
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (the pass kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization inside the solve graph):
+// a pass lets the next pass launch as soon as all its CTAs are resident, and
+// the next pass stages its static inputs (gx slab, pixel lists) before
+// waiting for the previous pass's fold / update to complete and become
+// visible.  Both are no-ops for a normal launch.
+__device__ __forceinline__ void hs_pdl_launch_next()
+{
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ void hs_pdl_wait_prev()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ double hs_wrap(double t)
 {
     // optics.py:31-45: exact fmod, then one exact +-2pi correction.

@@ -150,6 +150,8 @@ struct hs_plan {
     int32_t *d_tiles = nullptr;           // non-empty 64x32 tiles, packed (r0 << 16) | c0
     int32_t ntiles = 0;
     int num_sms = 148;
+    bool pdl = false;                     // next pass launch: programmatic dependent launch
+    bool pdl_enabled = true;              // HS_PDL=0 disables
     DevList storage;                      // storage order
     std::map<int, DevList> dense;         // full range, banded layout per slots-per-warp
     // compressed windows keyed (start, count, np): slab-ordered for np <= 128
@@ -584,7 +586,32 @@ FoldArgs fold_args(hs_plan *p, int32_t nchunks, const UpdArgs &u, int32_t lo = 0
     return f;
 }
 
-// Full-range fused pass with the GEMM-tile kernel (n <= 128).
+// Launch a pass kernel on the plan stream; inside a solve graph every pass
+// after the first is a programmatic dependent launch of the previous one
+// (hs_pdl_launch_next / hs_pdl_wait_prev in the kernels): its CTAs launch
+// and stage their static inputs while the previous pass folds.
+template <typename Arg>
+int launch_pass_kernel(hs_plan *p, void (*fn)(Arg), dim3 grid, dim3 block, size_t smem, const Arg &a)
+{
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = p->stream;
+    cudaLaunchAttribute attr[1];
+    if (p->pdl && p->pdl_enabled) {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    p->pdl = false;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, a));
+    return HS_OK;
+}
+
+// Full-range fused pass with the GEMM-tile kernels (hs_tile: n <= 128, hs_tilek: larger n).
 int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int32_t lo = 0, int32_t hi = -1,
                 unsigned char *raster = nullptr)
 {
@@ -614,9 +641,7 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     const size_t smem = chunked ? hs_tilek_smem_bytes() : hs_tile_smem_bytes(spt, p->n);
     if (hi <= lo) return HS_OK;
     dim3 grid(hi - lo, p->batch);
-    fn<<<grid, kThreads, smem, p->stream>>>(a);
-    CUDA_TRY(cudaGetLastError());
-    return HS_OK;
+    return launch_pass_kernel(p, fn, grid, dim3(kThreads), smem, a);
 }
 
 // Compressed-window pass over chunks [lo, hi) of a slab-ordered list.  A CTA
@@ -653,9 +678,8 @@ int launch_slab(hs_plan *p, int mode, const DevList &l, int32_t nchunks, const U
     }
     a.cpc = best;
     dim3 grid((unsigned)((span + best - 1) / best), p->batch);
-    hs_select_slab(c.ns)<<<grid, kSlabThreads, hs_slab_smem_bytes(c.np, l.sw), p->stream>>>(a);
-    CUDA_TRY(cudaGetLastError());
-    return HS_OK;
+    return launch_pass_kernel(p, hs_select_slab(c.ns), grid, dim3(kSlabThreads),
+                              hs_slab_smem_bytes(c.np, l.sw), a);
 }
 
 // One pass over `count` entries of list `l` starting at entry `off`.
@@ -759,10 +783,12 @@ int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags, doub
             u.iters = iters;
             mode = PM_BWD | PM_FWD;
         }
+        p->pdl = (j > 0);  // pass 0 follows the tables kernel (normal dependency)
         if (lst)
             rc = launch_pass(p, mode, *lst, 0, lst->count, 0, nullptr, nullptr, 0, u);
         else
             rc = full_pass(mode, u);
+        p->pdl = false;
         if (rc) return rc;
     }
     return HS_OK;
@@ -867,6 +893,7 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
         CUDA_TRY(cudaMemcpy(p->d_idx_img, p->h_index.data(), cells * sizeof(int32_t), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
+        if (const char *env = getenv("HS_PDL")) p->pdl_enabled = atoi(env) != 0;
         for (int ns = 1; ns <= 8; ++ns)
             CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_slab(ns),
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,

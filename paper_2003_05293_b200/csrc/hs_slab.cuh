@@ -155,8 +155,8 @@ __global__ void __launch_bounds__(32 * G, 1) hs_slab_kernel(const SlabArgs a)
     extern __shared__ float4 sm4[];
     __shared__ __align__(8) unsigned long long bar;
 
+    hs_pdl_launch_next();
     const int pat = blockIdx.y;
-    if (a.f.u.status[pat] != 0) return;
     const int q0 = a.f.chunk_base + blockIdx.x * a.cpc;
     const int nq = min(a.cpc, a.f.chunk_end - q0);
     const int tid = threadIdx.x;
@@ -175,7 +175,6 @@ __global__ void __launch_bounds__(32 * G, 1) hs_slab_kernel(const SlabArgs a)
     const uint32_t ent_a = hs_smem_addr(Ent);
     const uint32_t cf_a = hs_smem_addr(coef_s) + 8u * VEC * g;
 
-    for (int k = tid; k < NP; k += NT) coef_s[k] = a.coef[(int64_t)pat * NP + k];
     for (int k = tid; k < kSlabStreams * NP; k += NT) Es[k] = make_float2(0.f, 0.f);
 
     // per-warp entry staging: the warp's GPW streams of chunk q are the
@@ -300,7 +299,12 @@ __global__ void __launch_bounds__(32 * G, 1) hs_slab_kernel(const SlabArgs a)
     };
 
     __syncwarp();
-    stage(__ldg(a.chunk_c0 + q0));
+    stage(__ldg(a.chunk_c0 + q0));  // gx (tables) and lists: inputs of the whole solve
+    // -- everything below reads the previous pass's results (status, coef)
+    hs_pdl_wait_prev();
+    if (a.f.u.status[pat] != 0) return;  // uniform per CTA
+    for (int k = tid; k < NP; k += NT) coef_s[k] = a.coef[(int64_t)pat * NP + k];
+    __syncthreads();
     int rcur = -1;
     // smem address of this stream's entries in chunk buffer 0 / 1
     const uint32_t ent0 = ent_a + 8u * (stream * P), ent1 = ent0 + 8u * kSlabL;

@@ -86,9 +86,9 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tile_kernel(const TileArgs a)
     float2 *Bs = Vs;                   // [kTileC][kBS]   (after backward)
     float2 *Rs = Vs;                   // [32][KP]        (after forward)
 
+    hs_pdl_launch_next();
     const int pat = blockIdx.y;
     const int tile = a.f.chunk_base + blockIdx.x;
-    if (a.f.u.status[pat] != 0) return;
     const int tid = threadIdx.x;
     const int kb = hs_tile_kb(a.n);
     const int packed = __ldg(a.tiles + tile);
@@ -120,6 +120,9 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tile_kernel(const TileArgs a)
                 const int k = lane + 32 * m;
                 if (k < KP) Xs[k * kXS + warp + 8 * i] = v[i][m];
             }
+        // -- below: the previous pass's results (status, coef)
+        hs_pdl_wait_prev();
+        if (a.f.u.status[pat] != 0) return;  // uniform per CTA
         float2 w[MK];
 #pragma unroll
         for (int m = 0; m < MK; ++m) {

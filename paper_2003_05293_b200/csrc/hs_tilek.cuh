@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tilek_kernel(const TileArgs a)
     float2 *Bs = Vs + kKC * kVS;       // [kTileC][kBS]
     float2 *Rs = Vs;
 
+    hs_pdl_launch_next();
+    hs_pdl_wait_prev();  // coef / status of the previous pass
     const int pat = blockIdx.y;
     const int tile = a.f.chunk_base + blockIdx.x;
     if (a.f.u.status[pat] != 0) return;
