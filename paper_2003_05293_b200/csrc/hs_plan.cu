@@ -372,7 +372,7 @@ int build_slab_window(hs_plan *p, int64_t start, int64_t count, int np, DevList 
         CUDA_TRY(cudaMemcpy(out->chunk_c0, c0s.data(), c0s.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     out->count = (int64_t)ent.size();
-    out->chunk_len = kSlabL;
+    out->chunk_len = kSlabL / 2;  // fold units are half-chunks (16 streams)
     out->sorted_rows = 1;
     out->sw = sw;
     return HS_OK;
@@ -644,15 +644,18 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     return launch_pass_kernel(p, fn, grid, dim3(kThreads), smem, a);
 }
 
-// Compressed-window pass over chunks [lo, hi) of a slab-ordered list.  A CTA
-// streams cpc chunks (cpc | kGroup; chunk ranges are group-aligned): the
-// choice minimises waves x (cpc + staging cost) for this batch and never
-// changes results (each chunk keeps its own partial).
-int launch_slab(hs_plan *p, int mode, const DevList &l, int32_t nchunks, const UpdArgs &u, int32_t lo, int32_t hi)
+// Compressed-window pass over fold units [lo, hi) (half-chunks; lo, hi even)
+// of a slab-ordered list.  A whole-chunk CTA streams cpc chunks (cpc | 16;
+// unit ranges are fold-group-aligned), chosen to minimise waves x (cpc +
+// staging cost); when even one chunk per CTA leaves SMs idle (small
+// batches) each half-chunk gets its own CTA.  Every unit's partial is the
+// same sum either way, so the choice never changes results.
+int launch_slab(hs_plan *p, int mode, const DevList &l, int32_t nunits, const UpdArgs &u, int32_t lo, int32_t hi)
 {
     const Config &c = p->cfg;
     if (mode != (PM_BWD | PM_FWD)) return fail(HS_ECUDA, "slab window lists support the fused pass only");
-    if (nchunks > p->cap_chunks) return fail(HS_ECUDA, "fold buffers too small (%d chunks)", nchunks);
+    if (nunits > p->cap_chunks) return fail(HS_ECUDA, "fold buffers too small (%d units)", nunits);
+    if ((lo & 1) || (hi & 1)) return fail(HS_ECUDA, "slab unit range [%d, %d) splits a chunk", lo, hi);
     SlabArgs a;
     memset(&a, 0, sizeof a);
     a.ent = l.ent;
@@ -663,22 +666,25 @@ int launch_slab(hs_plan *p, int mode, const DevList &l, int32_t nchunks, const U
     a.gx = p->d_gx;
     a.gy = p->d_gy;
     a.coef = p->d_coef;
-    a.f = fold_args(p, nchunks, u, lo, hi);
-    const int64_t span = hi - lo;
+    a.f = fold_args(p, nunits, u, lo, hi);
+    const int64_t span = (hi - lo) / 2;  // chunks
+    const bool half = span * p->batch * 4 < (int64_t)p->num_sms * 3;
     int best = 1;
-    double best_cost = 1e300;
-    for (int cpc = 1; cpc <= kGroup; cpc *= 2) {
-        const int64_t ctas = (span + cpc - 1) / cpc * p->batch;
-        const int64_t waves = (ctas + p->num_sms - 1) / p->num_sms;
-        const double cost = (double)waves * (std::min<int64_t>(cpc, span) + 0.5);
-        if (cost < best_cost - 1e-9) {
-            best_cost = cost;
-            best = cpc;
+    if (!half) {
+        double best_cost = 1e300;
+        for (int cpc = 1; cpc <= kGroup / 2; cpc *= 2) {
+            const int64_t ctas = (span + cpc - 1) / cpc * p->batch;
+            const int64_t waves = (ctas + p->num_sms - 1) / p->num_sms;
+            const double cost = (double)waves * (std::min<int64_t>(cpc, span) + 0.5);
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                best = cpc;
+            }
         }
     }
     a.cpc = best;
-    dim3 grid((unsigned)((span + best - 1) / best), p->batch);
-    return launch_pass_kernel(p, hs_select_slab(c.ns), grid, dim3(kSlabThreads),
+    const dim3 grid(half ? (unsigned)(2 * span) : (unsigned)((span + best - 1) / best), p->batch);
+    return launch_pass_kernel(p, hs_select_slab(c.ns, half), grid, dim3(half ? kSlabThreads / 2 : kSlabThreads),
                               hs_slab_smem_bytes(c.np, l.sw), a);
 }
 
@@ -895,9 +901,10 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
         CUDA_TRY(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
         if (const char *env = getenv("HS_PDL")) p->pdl_enabled = atoi(env) != 0;
         for (int ns = 1; ns <= 8; ++ns)
-            CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_slab(ns),
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kSlabSmemBudget));  // process-wide cap: never lower it per plan
+            for (int h = 0; h < 2; ++h)
+                CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_slab(ns, h != 0),
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              kSlabSmemBudget));  // process-wide cap: never lower it per plan
         for (int w = 0; w < 2; ++w)
             CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_tilek(w != 0),
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs_tilek_smem_bytes()));
@@ -959,9 +966,10 @@ int hs_set_spots(hs_plan *p, int batch, int n, const double *x, const double *y,
     p->cfg = pick_config(n);
     const DevList *dense;
     if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
-    // slab windows: one chunk per kSlabL entries plus one padded tail per slab
+    // slab windows: two fold units per kSlabL-entry chunk, plus one padded
+    // tail chunk per slab
     const int64_t slab_chunks =
-        p->cfg.ns > 0 ? p->m / kSlabL + p->side / hs_slab_width(p->cfg.np, p->side) + 2 : 0;
+        p->cfg.ns > 0 ? 2 * (p->m / kSlabL + p->side / hs_slab_width(p->cfg.np, p->side) + 2) : 0;
     const int64_t chunks = std::max<int64_t>({(int64_t)geom_of(*dense, dense->count, p->cfg.spw).nchunks,
                                               (int64_t)kTargetChunks + 1, p->m / kMaxChunk + 2,
                                               (int64_t)p->ntiles, slab_chunks});

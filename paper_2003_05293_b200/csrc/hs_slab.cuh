@@ -142,28 +142,34 @@ __device__ __forceinline__ void hs_sts2(uint32_t addr, float2 v)
     asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
 }
 
-template <int NS, int G>
-__global__ void __launch_bounds__(32 * G, 1) hs_slab_kernel(const SlabArgs a)
+template <int NS, int G, bool HALF>
+__global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(const SlabArgs a)
 {
-    constexpr int NT = 32 * G;          // threads
+    constexpr int WPC = G;              // warps of a whole chunk (32 streams)
+    constexpr int NW = HALF ? WPC / 2 : WPC;  // warps in this CTA
+    constexpr int NT = 32 * NW;         // threads
     constexpr int GPW = 32 / G;         // pixel groups (streams) per warp
     constexpr int VEC = 16 / G;         // complex values per lane per shared load
     constexpr int NP = 16 * NS;
     constexpr int SPL = VEC * NS;       // spots per lane
     constexpr int P = kSlabP;
-    static_assert(GPW * (NT / 32) == kSlabStreams, "32 streams per CTA");
+    static_assert(GPW * WPC == kSlabStreams, "32 streams per chunk");
     extern __shared__ float4 sm4[];
     __shared__ __align__(8) unsigned long long bar;
 
     hs_pdl_launch_next();
     const int pat = blockIdx.y;
-    const int q0 = a.f.chunk_base + blockIdx.x * a.cpc;
-    const int nq = min(a.cpc, a.f.chunk_end - q0);
+    // fold units are half-chunks (16 streams); a whole-chunk CTA streams cpc
+    // chunks, a half-chunk CTA (small batches: twice the CTAs) one half
+    const int half = HALF ? (int)(blockIdx.x & 1) : 0;
+    const int q0 = a.f.chunk_base / 2 + (HALF ? (int)(blockIdx.x >> 1) : (int)blockIdx.x * a.cpc);
+    const int nq = HALF ? 1 : min(a.cpc, a.f.chunk_end / 2 - q0);
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
+    const int gw = warp + half * NW;    // warp index in the chunk layout
     const int g = lane & (G - 1), s = lane / G;
     const bool lo = g < G / 2;
-    const int stream = warp * GPW + s;
+    const int stream = gw * GPW + s;
 
     float2 *Xs = reinterpret_cast<float2 *>(sm4);                 // [sw][NP]
     float2 *Es = Xs + (size_t)a.sw * NP;                            // [32][NP]
@@ -185,12 +191,12 @@ __global__ void __launch_bounds__(32 * G, 1) hs_slab_kernel(const SlabArgs a)
         if (qi < nq)
 #pragma unroll
             for (int k = 0; k < EPL; ++k)
-                ent_reg[k] = __ldg(a.ent + (int64_t)(q0 + qi) * kSlabL + warp * GPW * P + lane + 32 * k);
+                ent_reg[k] = __ldg(a.ent + (int64_t)(q0 + qi) * kSlabL + gw * GPW * P + lane + 32 * k);
     };
     auto store_ent = [&](int qi) {
         if (qi < nq)
 #pragma unroll
-            for (int k = 0; k < EPL; ++k) Ent[(qi & 1) * kSlabL + warp * GPW * P + lane + 32 * k] = ent_reg[k];
+            for (int k = 0; k < EPL; ++k) Ent[(qi & 1) * kSlabL + gw * GPW * P + lane + 32 * k] = ent_reg[k];
     };
     fetch_ent(0);
     store_ent(0);
@@ -367,11 +373,10 @@ __global__ void __launch_bounds__(32 * G, 1) hs_slab_kernel(const SlabArgs a)
     auto chunk_end = [&](int qi) {
         if (rcur >= 0) flush();
         rcur = -1;
-        float2 *out = a.f.partials + (int64_t)pat * a.f.part_stride + (int64_t)(q0 + qi) * NP;
         // the warp's GPW streams: symmetric butterfly adds, kept in stream
-        // GPW w's row; then the warp rows summed in warp order
+        // GPW gw's row; then each half's 8 warp rows summed in warp order
         {
-            const uint32_t w0 = hs_smem_addr(Es) + 8u * (GPW * warp * NP + VEC * g);
+            const uint32_t w0 = hs_smem_addr(Es) + 8u * (GPW * gw * NP + VEC * g);
 #pragma unroll
             for (int j = 0; j < NS; ++j) {
                 f2x v[VEC];
@@ -395,17 +400,20 @@ __global__ void __launch_bounds__(32 * G, 1) hs_slab_kernel(const SlabArgs a)
             }
         }
         __syncthreads();
-        for (int k = tid; k < NP; k += NT) {
+        constexpr int HALVES = HALF ? 1 : 2;
+        for (int idx = tid; idx < HALVES * NP; idx += NT) {
+            const int hh = HALF ? half : idx / NP, k = HALF ? idx : idx - hh * NP;
             float x = 0.f, y = 0.f;
 #pragma unroll
-            for (int w = 0; w < NT / 32; ++w) {
-                const float2 v = Es[GPW * w * NP + k];
+            for (int w = 0; w < WPC / 2; ++w) {
+                const int row = GPW * (hh * (WPC / 2) + w) * NP + k;
+                const float2 v = Es[row];
                 x += v.x;
                 y += v.y;
+                Es[row] = make_float2(0.f, 0.f);
             }
-            out[k] = make_float2(x, y);
-#pragma unroll
-            for (int w = 0; w < NT / 32; ++w) Es[GPW * w * NP + k] = make_float2(0.f, 0.f);
+            a.f.partials[(int64_t)pat * a.f.part_stride + (int64_t)(2 * (q0 + qi) + hh) * NP + k] =
+                make_float2(x, y);
         }
         store_ent(qi + 2);  // chunk qi's buffer is consumed
         __syncwarp();
@@ -429,11 +437,11 @@ __global__ void __launch_bounds__(32 * G, 1) hs_slab_kernel(const SlabArgs a)
     }
     if (a.f.u.act != ACT_NONE) {
         __syncthreads();
-        hs_fold(a.f, pat, q0, reinterpret_cast<char *>(Es), nq);
+        hs_fold(a.f, pat, 2 * q0 + half, reinterpret_cast<char *>(Es), HALF ? 1 : 2 * nq);
     }
 }
 
 typedef void (*SlabFn)(SlabArgs);
-SlabFn hs_select_slab(int ns);
+SlabFn hs_select_slab(int ns, bool half);
 
 }  // namespace hs
