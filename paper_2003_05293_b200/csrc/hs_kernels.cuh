@@ -123,6 +123,21 @@ __device__ __forceinline__ double hs_wrap(double t)
     return w;
 }
 
+// Stored phase of a pixel: arg S from fp32 atan2f, widened to f64 and wrapped
+// to [-pi, pi) with pi -> -pi (optics.py:31-45, solvers.py:96-101), arg(0) =
+// 0.  atan2f's range is [-pi_f32, pi_f32] and pi_f32 > pi_f64, so the only
+// widened values outside [-pi, pi) are +-pi_f32 themselves: the wrap is
+// decided in fp32 and its two results are the fp64 constants pi_f32 - 2 pi
+// and -pi_f32 + 2 pi (the same bits as wrapping the widened value).
+__device__ __forceinline__ double hs_phase_f64(float x, float y)
+{
+    if (x == 0.f && y == 0.f) return 0.0;
+    const float p = atan2f(y, x);
+    if (p == 3.14159274101257324f) return 3.14159274101257324 - kTwoPi;
+    if (p == -3.14159274101257324f) return -3.14159274101257324 + kTwoPi;
+    return (double)p;
+}
+
 // Linear phase -> gray lookup of the default PhaseLut (fileio.py:159-213):
 // g = rint((p + pi) * 256 / (2 pi)) mod 256 on the wrapped fp64 phase, with
 // the reference's operation order (no contraction), so a device raster equals
@@ -533,12 +548,7 @@ hs_pass_kernel(const PassArgs a)
             if (WRITE && valid && g == 0) {
                 const int64_t di = a.dst ? (int64_t)a.dst[i] : i + a.idx_base;
                 if (di >= 0) {
-                    double ph = 0.0;
-                    if (sr != 0.f || si != 0.f) {
-                        ph = (double)atan2f(si, sr);
-                        if (ph >= kPi) ph -= kTwoPi;       // pi -> -pi convention
-                        else if (ph < -kPi) ph += kTwoPi;  // fp32 -pi lies below fp64 -pi
-                    }
+                    const double ph = hs_phase_f64(sr, si);
                     a.phase_out[(int64_t)pat * a.phase_stride + di] = ph;
                     if (a.raster)
                         a.raster[(int64_t)pat * a.side * a.side + (int64_t)(rc >> 16) * a.side + (rc & 0xffff)] =

@@ -144,12 +144,7 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tilek_kernel(const TileArgs a)
             if (WRITE && in) {
                 const int32_t di = __ldg(a.idx_img + gidx);
                 if (di >= 0) {
-                    double ph = 0.0;
-                    if (x != 0.f || y != 0.f) {
-                        ph = (double)atan2f(y, x);
-                        if (ph >= kPi) ph -= kTwoPi;       // pi -> -pi convention
-                        else if (ph < -kPi) ph += kTwoPi;  // fp32 -pi lies below fp64 -pi
-                    }
+                    const double ph = hs_phase_f64(x, y);
                     a.phase_out[(int64_t)pat * a.phase_stride + di] = ph;
                     if (a.raster) a.raster[(int64_t)pat * a.side * a.side + gidx] = hs_gray_linear(ph);
                 }
