@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tile_kernel(const TileArgs a)
 #pragma unroll
         for (int j = 0; j < 4; ++j) sacc[i][j] = 0ull;
     const f2x *X2 = reinterpret_cast<const f2x *>(Xs);
-#pragma unroll 2
+#pragma unroll 16
     for (int k = 0; k < kb; ++k) {
         const float4 v01 = *reinterpret_cast<const float4 *>(Vs + k * kVS + 4 * tr);
         const float4 v23 = *reinterpret_cast<const float4 *>(Vs + k * kVS + 4 * tr + 2);
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tile_kernel(const TileArgs a)
     f2x t0[SPT], t1[SPT];
 #pragma unroll
     for (int j = 0; j < SPT; ++j) t0[j] = t1[j] = 0ull;
-#pragma unroll 2
+#pragma unroll 16
     for (int c = 0; c < kTileC; ++c) {
         const float4 b = *reinterpret_cast<const float4 *>(Bs + c * kBS + 2 * rg);
         f2x x[SPT];
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tile_kernel(const TileArgs a)
     for (int k = tid; k < a.np; k += kThreads) {
         float x = 0.f, y = 0.f;
         if (k < KP) {
-#pragma unroll 8
+#pragma unroll 16
             for (int q = 0; q < 32; ++q) {
                 const float2 v = Rs[q * KP + k];
                 x += v.x;

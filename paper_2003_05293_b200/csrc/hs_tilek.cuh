@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tilek_kernel(const TileArgs a)
         stage_x(ch * kKC);
         stage_v(ch * kKC);
         __syncthreads();
-#pragma unroll 2
+#pragma unroll 16
         for (int k = 0; k < kKC; ++k) {
             const float4 v01 = *reinterpret_cast<const float4 *>(Vs + k * kVS + 4 * tr);
             const float4 v23 = *reinterpret_cast<const float4 *>(Vs + k * kVS + 4 * tr + 2);
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tilek_kernel(const TileArgs a)
         f2x t0[8], t1[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) t0[j] = t1[j] = 0ull;
-#pragma unroll 2
+#pragma unroll 16
         for (int c = 0; c < kTileC; ++c) {
             const float4 b = *reinterpret_cast<const float4 *>(Bs + c * kBS + 2 * rg);
             f2x x[8];
