@@ -429,9 +429,9 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
     for (int qi = 0; qi < nq; ++qi) {
         fetch_ent(qi + 2);
 #pragma unroll 1
-        for (int t = 0; t < P; t += 4) {
-            pair(qi, t);
-            pair(qi, t + 2);
+        for (int t = 0; t < P; t += 16) {
+#pragma unroll
+            for (int u = 0; u < 16; u += 2) pair(qi, t + u);
         }
         chunk_end(qi);
     }
