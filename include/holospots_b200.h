@@ -182,6 +182,26 @@ int hs_shard_pass(hs_plan *plan, int pass, double *local_groups, int *g_lo, int 
 int hs_shard_update(hs_plan *plan, int pass, const double *all_groups, int ngroups);
 /* Group range [g_lo, g_hi) of this rank and the total group count of pass j. */
 int hs_shard_groups(hs_plan *plan, int pass, int *g_lo, int *g_hi, int *ngroups);
+
+/* The same sharded solve with the exchange over peer memory (NVLink P2P
+ * through CUDA IPC) instead of a host round trip per pass
+ * (csrc/hs_xchg.cuh).  After hs_shard_begin:
+ *   hs_shard_p2p_setup(handle)            this rank's exchange buffer; writes
+ *                                         its cudaIpcMemHandle (HS_IPC_HANDLE_BYTES)
+ *   handles = all-gather(handle)          rank order, caller (once per solve)
+ *   hs_shard_p2p_open(handles)            maps the peers' buffers
+ *   for j: hs_shard_p2p_pass(j)           enqueues the rank's chunk range, the
+ *                                         publish of its group partials into every
+ *                                         rank's buffer and the gather + update;
+ *                                         no host synchronisation
+ *   hs_sync(); hs_shard_p2p_close()
+ * Results are bitwise identical to hs_shard_pass / hs_shard_update and to
+ * hs_solve.  A peer that never publishes times out after ~2 s (status 5). */
+#define HS_IPC_HANDLE_BYTES 64
+int hs_shard_p2p_setup(hs_plan *plan, unsigned char *ipc_handle_out);
+int hs_shard_p2p_open(hs_plan *plan, const unsigned char *ipc_handles);
+int hs_shard_p2p_pass(hs_plan *plan, int pass);
+int hs_shard_p2p_close(hs_plan *plan);
 int hs_padded_spots(hs_plan *plan);
 
 /* Instrumentation for bench.py: the plan's cudaStream_t, the number of

@@ -45,7 +45,10 @@ EXPORTS = (
     "hs_last_launch_count", "hs_time_kernel", "hs_fma_peak", "hs_host_alloc",
     "hs_host_free", "hs_probe", "hs_solve_host_async", "hs_shard_begin", "hs_shard_pass",
     "hs_shard_update", "hs_padded_spots", "hs_shard_groups", "hs_raster", "hs_get_raster",
+    "hs_shard_p2p_setup", "hs_shard_p2p_open", "hs_shard_p2p_pass", "hs_shard_p2p_close",
 )
+
+IPC_HANDLE_BYTES = 64  # HS_IPC_HANDLE_BYTES
 
 _lib = None
 _lock = threading.Lock()
@@ -97,6 +100,10 @@ def load():
             "hs_probe": (I, [P, P, I64, P, I, P]),
             "hs_host_alloc": (P, [I64]),
             "hs_host_free": (None, [P]),
+            "hs_shard_p2p_setup": (I, [P, P]),
+            "hs_shard_p2p_open": (I, [P, P]),
+            "hs_shard_p2p_pass": (I, [P, I]),
+            "hs_shard_p2p_close": (I, [P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -293,6 +300,26 @@ class Plan:
     def shard_update(self, j: int, all_groups: np.ndarray) -> None:
         g = np.ascontiguousarray(all_groups, dtype=np.complex128)
         check(load().hs_shard_update(self.handle, j, ptr(g), g.shape[1]))
+
+    # ---- the same over peer memory (csrc/hs_xchg.cuh) -------------------
+    def p2p_setup(self) -> bytes:
+        """Allocate this rank's exchange buffer; returns its CUDA IPC handle."""
+        buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        check(load().hs_shard_p2p_setup(self.handle, buf))
+        return buf.raw
+
+    def p2p_open(self, handles) -> None:
+        """Map the world's exchange buffers (handles in rank order)."""
+        blob = b"".join(bytes(h) for h in handles)
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        check(load().hs_shard_p2p_open(self.handle, buf))
+
+    def p2p_pass(self, j: int) -> None:
+        """Enqueue pass j (chunk range + peer publish + gather/update); async."""
+        check(load().hs_shard_p2p_pass(self.handle, j))
+
+    def p2p_close(self) -> None:
+        check(load().hs_shard_p2p_close(self.handle))
 
     def padded_spots(self) -> int:
         return int(load().hs_padded_spots(self.handle))

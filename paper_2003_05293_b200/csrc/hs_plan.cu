@@ -24,6 +24,7 @@
 #include "hs_kernels.cuh"
 #include "hs_tile.cuh"
 #include "hs_tilek.cuh"
+#include "hs_xchg.cuh"
 #include "hs_slab.cuh"
 
 using namespace hs;
@@ -191,6 +192,18 @@ struct hs_plan {
         int rank = 0, world = 1, alg = 0, iters = 0, cs = 0, passes = 0;
         int64_t subset = 0, half = 1;
     } shard;
+    // peer-memory exchange of the row-sharded solve (hs_shard_p2p_*)
+    struct {
+        char *local = nullptr;            // this rank's buffer: flags | xbuf
+        size_t bytes = 0;
+        int ngmax = 0;
+        std::vector<char *> bases;        // [world] mapped buffer bases (own + peers)
+        double2 **d_xbuf = nullptr;       // [world] device array of xbuf pointers
+        unsigned long long **d_flags = nullptr;
+        int32_t *d_cnt = nullptr;
+        uint64_t epoch = 0;
+        bool open = false;
+    } xchg;
     int64_t last_launches = 0;
     std::map<std::tuple<int, int, int64_t, int, int, int>, cudaGraphExec_t> graphs;
 };
@@ -936,6 +949,7 @@ void hs_plan_destroy(hs_plan *p)
 {
     if (!p) return;
     cudaSetDevice(p->device);
+    hs_shard_p2p_close(p);
     cudaStreamSynchronize(p->stream);
     cudaStreamSynchronize(p->copy_stream);
     free_batch(p);
@@ -1382,6 +1396,138 @@ int hs_shard_pass(hs_plan *p, int j, double *groups, int *g_lo, int *g_hi, int *
                                        sizeof(double2) * cnt * np, p->batch, cudaMemcpyDeviceToHost, p->stream));
     }
     return sync_and_check(p);
+}
+
+// ---- peer-memory exchange (hs_xchg.cuh): the sharded solve without host
+// round trips.  Buffer = flags [world] (256-B padded) | xbuf [2][B][ngmax][np].
+static const size_t kFlagBytes = 256;
+
+int hs_shard_p2p_setup(hs_plan *p, unsigned char *handle_out)
+{
+    auto &sh = p->shard;
+    auto &x = p->xchg;
+    if (!sh.active) return fail(HS_EINVAL, "hs_shard_begin first");
+    if ((size_t)sh.world * 8 > kFlagBytes) return fail(HS_EINVAL, "world %d too large", sh.world);
+    int rc;
+    if ((rc = check_device(p))) return rc;
+    hs_shard_p2p_close(p);
+    x.ngmax = (int)((p->cap_chunks + kGroup - 1) / kGroup);
+    x.bytes = kFlagBytes + sizeof(double2) * (size_t)2 * p->batch * x.ngmax * p->cfg.np;
+    CUDA_TRY(cudaMalloc((void **)&x.local, x.bytes));
+    CUDA_TRY(cudaMemset(x.local, 0, kFlagBytes));
+    CUDA_TRY(cudaDeviceSynchronize());
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, x.local));
+    memcpy(handle_out, &h, sizeof h);
+    if ((rc = dalloc(&x.d_cnt, 1))) return rc;
+    CUDA_TRY(cudaMemset(x.d_cnt, 0, sizeof(int32_t)));
+    x.epoch = 0;
+    return HS_OK;
+}
+
+int hs_shard_p2p_open(hs_plan *p, const unsigned char *handles)
+{
+    auto &sh = p->shard;
+    auto &x = p->xchg;
+    if (!x.local) return fail(HS_EINVAL, "hs_shard_p2p_setup first");
+    int rc;
+    if ((rc = check_device(p))) return rc;
+    x.bases.assign(sh.world, nullptr);
+    for (int r = 0; r < sh.world; ++r) {
+        if (r == sh.rank) {
+            x.bases[r] = x.local;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, handles + (size_t)r * sizeof h, sizeof h);
+        void *ptr = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        x.bases[r] = (char *)ptr;
+    }
+    std::vector<double2 *> xb(sh.world);
+    std::vector<unsigned long long *> fl(sh.world);
+    for (int r = 0; r < sh.world; ++r) {
+        fl[r] = (unsigned long long *)x.bases[r];
+        xb[r] = (double2 *)(x.bases[r] + kFlagBytes);
+    }
+    if ((rc = dalloc(&x.d_xbuf, sh.world)) || (rc = dalloc(&x.d_flags, sh.world))) return rc;
+    CUDA_TRY(cudaMemcpy(x.d_xbuf, xb.data(), sizeof(double2 *) * sh.world, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(x.d_flags, fl.data(), sizeof(void *) * sh.world, cudaMemcpyHostToDevice));
+    x.open = true;
+    return HS_OK;
+}
+
+// Enqueue pass j: the rank's chunk range, the peer publish of its groups and
+// the gather + update.  Asynchronous: the device does the waiting.
+int hs_shard_p2p_pass(hs_plan *p, int j)
+{
+    auto &sh = p->shard;
+    auto &x = p->xchg;
+    if (!sh.active || j < 0 || j >= sh.passes) return fail(HS_EINVAL, "shard pass %d out of range", j);
+    if (!x.open) return fail(HS_EINVAL, "hs_shard_p2p_open first");
+    int rc, kind, nch;
+    const DevList *lst;
+    if ((rc = check_device(p)) || (rc = shard_pass_desc(p, j, &kind, &lst, &nch))) return rc;
+    int lo, hi;
+    shard_range(nch, sh.rank, sh.world, &lo, &hi);
+    const bool last = (j == sh.passes - 1);
+    const int mode = last ? (PM_BWD | PM_FWD | PM_WRITE) : (PM_BWD | PM_FWD);
+    const UpdArgs none = upd_args(p, ACT_NONE);
+    if (kind == 0)
+        rc = launch_tile(p, last, none, p->d_out[0], lo, hi);
+    else
+        rc = launch_pass(p, mode, *lst, 0, lst->count, 0, nullptr, last ? p->d_out[0] : nullptr, p->m, none, lo, hi);
+    if (rc) return rc;
+    const int ng = (nch + kGroup - 1) / kGroup;
+    if (ng > x.ngmax) return fail(HS_ECUDA, "exchange buffer too small (%d groups)", ng);
+    UpdArgs u = upd_args(p, last ? ACT_FINAL : ACT_STEP);
+    u.iter = j;
+    u.iters = std::max(sh.iters, 1);
+    XchgArgs a;
+    memset(&a, 0, sizeof a);
+    a.f = fold_args(p, nch, u, lo, hi);
+    a.g_lo = lo / kGroup;
+    a.g_hi = (hi + kGroup - 1) / kGroup;
+    a.ngroups = ng;
+    a.ngmax = x.ngmax;
+    a.world = sh.world;
+    a.rank = sh.rank;
+    a.slot = j & 1;
+    a.epoch = ++x.epoch;
+    a.peer_xbuf = x.d_xbuf;
+    a.peer_flags = x.d_flags;
+    a.flags_local = (unsigned long long *)x.local;
+    a.xbuf_local = (const double2 *)(x.local + kFlagBytes);
+    a.pub_cnt = x.d_cnt;
+    if (a.g_hi > a.g_lo) {
+        hs_publish_kernel<<<dim3(a.g_hi - a.g_lo, p->batch), 128, 0, p->stream>>>(a);
+        CUDA_TRY(cudaGetLastError());
+    } else {  // a rank without groups still announces the epoch
+        XchgArgs b = a;
+        b.announce_only = 1;
+        hs_publish_kernel<<<dim3(1, 1), 128, 0, p->stream>>>(b);
+        CUDA_TRY(cudaGetLastError());
+    }
+    hs_gather_update_kernel<<<p->batch, kThreads, sizeof(double2) * 3 * p->cfg.np, p->stream>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    if (last) sh.active = false;
+    return HS_OK;
+}
+
+int hs_shard_p2p_close(hs_plan *p)
+{
+    auto &x = p->xchg;
+    if (x.local) cudaStreamSynchronize(p->stream);
+    for (size_t r = 0; r < x.bases.size(); ++r)
+        if (x.bases[r] && x.bases[r] != x.local) cudaIpcCloseMemHandle(x.bases[r]);
+    x.bases.clear();
+    if (x.local) cudaFree(x.local);
+    x.local = nullptr;
+    dfree(x.d_xbuf);
+    dfree(x.d_flags);
+    dfree(x.d_cnt);
+    x.open = false;
+    return HS_OK;
 }
 
 int hs_shard_groups(hs_plan *p, int j, int *g_lo, int *g_hi, int *ngroups)

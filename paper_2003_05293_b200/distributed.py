@@ -82,14 +82,19 @@ def sharded_fields(partials: np.ndarray, world: int, rank: int, all_gather) -> n
 
 
 # ---------------------------------------------------------------- device path
-def solve_sharded(pupil, spots, config, rank: int, world: int, all_gather, device=None):
+def solve_sharded(pupil, spots, config, rank: int, world: int, all_gather, device=None,
+                  exchange: str = "host"):
     """Row-sharded solve of one pattern across ``world`` processes.
 
-    Every rank calls this with the same ``spots`` / ``config``;
-    ``all_gather(obj) -> list`` (rank order) exchanges the per-pass group
-    partials (``ngroups x np`` complex128 per pass) and finally the phase
-    slabs.  Returns ``(Hologram, SolverTrace)`` identical on every rank and
-    bitwise equal to :func:`paper_2003_05293_b200.solve` on one GPU.
+    Every rank calls this with the same ``spots`` / ``config``.
+    ``exchange="host"``: ``all_gather(obj) -> list`` (rank order) exchanges
+    the per-pass group partials (``ngroups x np`` complex128 per pass).
+    ``exchange="p2p"``: the ranks swap CUDA IPC handles once through
+    ``all_gather`` and every pass exchanges its group partials over peer
+    memory on the device (csrc/hs_xchg.cuh) -- no host round trip.  Either
+    way the phase slabs are gathered at the end, and the result
+    ``(Hologram, SolverTrace)`` is identical on every rank and bitwise equal
+    to :func:`paper_2003_05293_b200.solve` on one GPU.
     """
     import time
 
@@ -111,14 +116,27 @@ def solve_sharded(pupil, spots, config, rank: int, world: int, all_gather, devic
     plan.shard_begin(_ALG_CODE[config.algorithm], iters, subset, _theta0(config.seed, n),
                      rank, world)
     passes = 1 if config.algorithm == "rs" else iters + 1
-    for j in range(passes):
-        local, g_lo, g_hi, ngroups = plan.shard_pass(j)
-        pieces = all_gather((g_lo, g_hi, local))
-        order = sorted(pieces, key=lambda t: t[0])
-        groups = np.concatenate([t[2] for t in order if t[2].shape[1]], axis=1)
-        if groups.shape[1] != ngroups:
-            raise RuntimeError(f"group exchange incomplete: {groups.shape[1]} of {ngroups}")
-        plan.shard_update(j, groups)
+    if exchange == "p2p":
+        handles = all_gather(plan.p2p_setup())
+        try:
+            plan.p2p_open(handles)
+            for j in range(passes):
+                plan.p2p_pass(j)
+            plan.sync()
+        finally:
+            all_gather(None)  # every rank finished reading its peers' buffers
+            plan.p2p_close()
+    elif exchange == "host":
+        for j in range(passes):
+            local, g_lo, g_hi, ngroups = plan.shard_pass(j)
+            pieces = all_gather((g_lo, g_hi, local))
+            order = sorted(pieces, key=lambda t: t[0])
+            groups = np.concatenate([t[2] for t in order if t[2].shape[1]], axis=1)
+            if groups.shape[1] != ngroups:
+                raise RuntimeError(f"group exchange incomplete: {groups.shape[1]} of {ngroups}")
+            plan.shard_update(j, groups)
+    else:
+        raise ValueError(f"unknown exchange {exchange!r}")
     status, deg = plan.status()
     _raise_status(int(status[0]))
     mine = plan.phases()[0]

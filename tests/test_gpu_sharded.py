@@ -32,7 +32,7 @@ def _spots(n, seed):
     return hs.random_foci(n, seed, xy=8e-5, z=3e-5)
 
 
-def _worker(rank, world, port, case, out):
+def _worker(rank, world, port, case, out, exchange="host"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -45,7 +45,8 @@ def _worker(rank, world, port, case, out):
             dist.all_gather_object(res, obj)
             return res
 
-        holo, trace = D.solve_sharded(pupil, _spots(n, 11), cfg, rank, world, all_gather, device=0)
+        holo, trace = D.solve_sharded(pupil, _spots(n, 11), cfg, rank, world, all_gather, device=0,
+                                      exchange=exchange)
         np.savez(f"{out}.{rank}.npz", phase=holo.phase, e=trace.quality.efficiency,
                  u=trace.quality.uniformity,
                  mags=np.array([r.magnitudes for r in trace.records]).reshape(-1),
@@ -54,10 +55,13 @@ def _worker(rank, world, port, case, out):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("exchange", ["host", "p2p"])
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_two_rank_sharded_solve_bitwise(tmp_path, case):
+def test_two_rank_sharded_solve_bitwise(tmp_path, case, exchange):
+    """host: group partials through gloo; p2p: through CUDA IPC peer memory
+    written by the publish kernel (two processes share the one GPU here)."""
     out = str(tmp_path / "res")
-    mp.spawn(_worker, args=(2, _free_port(), case, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), case, out, exchange), nprocs=2, join=True)
     pk, n, alg, iters, c = CASES[case]
     pupil = hs.build_pupil(**pk)
     holo, trace = hs.solve(pupil, _spots(n, 11), hs.SolverConfig(alg, iters, c, seed=5))
