@@ -83,15 +83,16 @@ def sharded_fields(partials: np.ndarray, world: int, rank: int, all_gather) -> n
 
 # ---------------------------------------------------------------- device path
 def solve_sharded(pupil, spots, config, rank: int, world: int, all_gather, device=None,
-                  exchange: str = "host"):
+                  exchange: str = "p2p"):
     """Row-sharded solve of one pattern across ``world`` processes.
 
     Every rank calls this with the same ``spots`` / ``config``.
-    ``exchange="host"``: ``all_gather(obj) -> list`` (rank order) exchanges
-    the per-pass group partials (``ngroups x np`` complex128 per pass).
-    ``exchange="p2p"``: the ranks swap CUDA IPC handles once through
+    ``exchange="p2p"`` (default, one node): the ranks swap CUDA IPC handles once through
     ``all_gather`` and every pass exchanges its group partials over peer
-    memory on the device (csrc/hs_xchg.cuh) -- no host round trip.  Either
+    memory on the device (csrc/hs_xchg.cuh) -- no host round trip.
+    ``exchange="host"`` (e.g. across nodes): ``all_gather(obj) -> list``
+    (rank order) carries the per-pass group partials (``ngroups x np``
+    complex128 per pass) through the host.  Either
     way the phase slabs are gathered at the end, and the result
     ``(Hologram, SolverTrace)`` is identical on every rank and bitwise equal
     to :func:`paper_2003_05293_b200.solve` on one GPU.
