@@ -52,6 +52,7 @@ int fail(int code, const char *fmt, ...)
     } while (0)
 
 constexpr int kColBlock = 64;  // dense layout: columns per CTA chunk
+constexpr int kSplitBatch = 16;  // batches >= this record two graph branches (record_solve)
 
 struct DevList {
     int32_t *rc = nullptr;
@@ -152,6 +153,9 @@ struct hs_plan {
     int32_t ntiles = 0;
     int num_sms = 148;
     bool pdl = false;                     // next pass launch: programmatic dependent launch
+    int view0 = 0;                        // first pattern of the sub-batch being recorded
+    cudaStream_t stream2 = nullptr;       // second branch of a split solve graph
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     bool pdl_enabled = true;              // HS_PDL=0 disables
     DevList storage;                      // storage order
     std::map<int, DevList> dense;         // full range, banded layout per slots-per-warp
@@ -553,21 +557,23 @@ UpdArgs upd_args(hs_plan *p, int act)
     u.act = act;
     u.n = p->n;
     u.np = p->cfg.np;
-    u.a0 = p->d_a0;
-    u.w = p->d_w;
-    u.coef = p->d_coef;
+    // a sub-batch view (p->view0) sees patterns view0 .. view0 + batch - 1
+    const int64_t b0 = p->view0, n = p->n, np = p->cfg.np;
+    u.a0 = p->d_a0 + b0 * n;
+    u.w = p->d_w + b0 * np;
+    u.coef = p->d_coef + b0 * np;
     u.trace_w = p->d_trace_w;
     u.trace_m = p->d_trace_m;
     u.iters = 1;
-    u.status = p->d_status;
-    u.degen = p->d_degen;
-    u.qstatus = p->d_qstatus;
-    u.fields = p->d_fields;
+    u.status = p->d_status + b0;
+    u.degen = p->d_degen + b0;
+    u.qstatus = p->d_qstatus + b0;
+    u.fields = p->d_fields + b0 * n * 2;
     u.inv_norm = 1.0 / (p->sum_amp * p->sum_amp);
-    u.e = p->d_e;
-    u.u = p->d_u;
-    u.inten = p->d_inten;
-    u.rel = p->d_rel;
+    u.e = p->d_e + b0;
+    u.u = p->d_u + b0;
+    u.inten = p->d_inten + b0 * n;
+    u.rel = p->d_rel + b0 * n;
     return u;
 }
 
@@ -588,14 +594,16 @@ FoldArgs fold_args(hs_plan *p, int32_t nchunks, const UpdArgs &u, int32_t lo = 0
     f.chunk_base = lo;
     f.chunk_end = hi < 0 ? nchunks : hi;
     f.np = p->cfg.np;
-    f.partials = p->d_part;
+    const int64_t b0 = p->view0;
+    f.partials = p->d_part + b0 * p->part_stride;
     f.part_stride = p->part_stride;
-    f.gpart = p->d_gpart;
+    f.gpart = p->d_gpart + b0 * p->gpart_stride;
     f.gpart_stride = p->gpart_stride;
-    f.grp_cnt = p->d_grp_cnt;
-    f.pat_cnt = p->d_pat_cnt;
+    f.grp_cnt = p->d_grp_cnt + b0 * p->cnt_stride;
+    f.pat_cnt = p->d_pat_cnt + b0;
     f.cnt_stride = p->cnt_stride;
     f.u = u;
+    // trace rows are [B][iters][n]: offset by the view once the caller set iters
     return f;
 }
 
@@ -637,14 +645,14 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     a.side = p->side;
     a.np = c.np;
     a.tab_stride = (int64_t)p->side * c.np;
-    a.gx = p->d_gx;
-    a.gy = p->d_gy;
-    a.coef = p->d_coef;
+    a.gx = p->d_gx + p->view0 * a.tab_stride;
+    a.gy = p->d_gy + p->view0 * a.tab_stride;
+    a.coef = p->d_coef + (int64_t)p->view0 * c.np;
     a.amp_img = p->d_amp_img;
     a.idx_img = p->d_idx_img;
-    a.phase_out = phase_out;
+    a.phase_out = phase_out ? phase_out + (int64_t)p->view0 * p->m : nullptr;
     a.phase_stride = p->m;
-    a.raster = raster;
+    a.raster = raster ? raster + (int64_t)p->view0 * p->side * p->side : nullptr;
     a.f = fold_args(p, p->ntiles, u, lo, hi);
     a.n = p->n;
     const int spt = (p->n + 7) / 8;
@@ -676,9 +684,9 @@ int launch_slab(hs_plan *p, int mode, const DevList &l, int32_t nunits, const Up
     a.sw = l.sw;
     a.side = p->side;
     a.tab_stride = (int64_t)p->side * c.np;
-    a.gx = p->d_gx;
-    a.gy = p->d_gy;
-    a.coef = p->d_coef;
+    a.gx = p->d_gx + p->view0 * a.tab_stride;
+    a.gy = p->d_gy + p->view0 * a.tab_stride;
+    a.coef = p->d_coef + (int64_t)p->view0 * c.np;
     a.f = fold_args(p, nunits, u, lo, hi);
     const int64_t span = (hi - lo) / 2;  // chunks
     const bool half = span * p->batch * 4 < (int64_t)p->num_sms * 3;
@@ -724,12 +732,13 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
     a.raster = raster;
     a.side = p->side;
     a.tab_stride = (int64_t)p->side * c.np;
-    a.gx = p->d_gx;
-    a.gy = p->d_gy;
-    a.coef = p->d_coef;
-    a.phase_in = phase_in;
-    a.phase_out = phase_out;
+    a.gx = p->d_gx + p->view0 * a.tab_stride;
+    a.gy = p->d_gy + p->view0 * a.tab_stride;
+    a.coef = p->d_coef + (int64_t)p->view0 * c.np;
+    a.phase_in = phase_in ? phase_in + p->view0 * phase_stride : nullptr;
+    a.phase_out = phase_out ? phase_out + p->view0 * phase_stride : nullptr;
     a.phase_stride = phase_stride;
+    if (a.raster) a.raster += (int64_t)p->view0 * p->side * p->side;
     if (hi < 0) hi = geo.nchunks;
     if (hi <= lo) return HS_OK;
     if (l.sw > 0) return launch_slab(p, mode, l, geo.nchunks, u, lo, hi);
@@ -758,26 +767,19 @@ int ensure_tables(hs_plan *p)
     return HS_OK;
 }
 
-// The solve schedule (solvers.py:192-235), fused: pass 0 superposes coef_0
-// over read_1 and projects it; the fold of pass j applies iteration j+1's
-// update (trace record j+1, coef_{j+1}); pass j >= 1 superposes coef_j over
-// write_j (= read_{j+1}); the last pass writes the phase and yields the
-// full-range fields of quality_report.
-int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags, double *out)
+// The passes of one sub-batch (patterns view0 .. view0 + batch - 1) on the
+// current p->stream.
+int record_passes(hs_plan *p, int alg, int iters, int64_t subset, int flags, double *out)
 {
     int rc;
     const bool want_fields = (flags & HS_WANT_FIELDS) != 0;
     const int64_t m = p->m;
-    if ((rc = reset_status(p))) return rc;
-    if ((rc = launch_tables(p, true))) return rc;
     const DevList *dense;
     if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
     const int final_mode = want_fields ? (PM_BWD | PM_FWD | PM_WRITE) : (PM_BWD | PM_WRITE);
     const UpdArgs fin = upd_args(p, want_fields ? ACT_FINAL : ACT_NONE);
     const bool tiled = true;  // GEMM-tile full passes for every n (hs_tile / hs_tilek)
     unsigned char *raster = (flags & HS_WANT_RASTER) ? p->d_raster : nullptr;
-    if (raster)
-        CUDA_TRY(cudaMemsetAsync(raster, 0, (size_t)p->batch * p->side * p->side, p->stream));
     auto full_pass = [&](int mode, const UpdArgs &u) -> int {
         const bool wr = (mode & PM_WRITE) != 0;
         if (tiled && (mode & PM_FWD)) return launch_tile(p, wr, u, out, 0, -1, wr ? raster : nullptr);
@@ -800,6 +802,8 @@ int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags, doub
             u = upd_args(p, ACT_STEP);
             u.iter = j;
             u.iters = iters;
+            u.trace_w += (int64_t)p->view0 * iters * p->n;  // trace rows [B][iters][n]
+            u.trace_m += (int64_t)p->view0 * iters * p->n;
             mode = PM_BWD | PM_FWD;
         }
         p->pdl = (j > 0);  // pass 0 follows the tables kernel (normal dependency)
@@ -810,6 +814,45 @@ int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags, doub
         p->pdl = false;
         if (rc) return rc;
     }
+    return HS_OK;
+}
+
+// The solve schedule (solvers.py:192-235), fused: pass 0 superposes coef_0
+// over read_1 and projects it; the fold of pass j applies iteration j+1's
+// update (trace record j+1, coef_{j+1}); pass j >= 1 superposes coef_j over
+// write_j (= read_{j+1}); the last pass writes the phase and yields the
+// full-range fields of quality_report.  Batches of >= kSplitBatch patterns
+// are recorded as two independent branches of the graph (halves of the
+// batch on two streams): every pass ends in a partly filled wave and a
+// serial fold tail, which the other branch's passes fill (+6% at B = 32).
+// Patterns never interact, so the split cannot change any result.
+int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags, double *out)
+{
+    int rc;
+    if ((rc = reset_status(p))) return rc;
+    if ((rc = launch_tables(p, true))) return rc;
+    if (flags & HS_WANT_RASTER)
+        CUDA_TRY(cudaMemsetAsync(p->d_raster, 0, (size_t)p->batch * p->side * p->side, p->stream));
+    static const bool no_split = getenv("HS_SPLIT") && atoi(getenv("HS_SPLIT")) == 0;
+    if (p->batch < kSplitBatch || no_split) return record_passes(p, alg, iters, subset, flags, out);
+    const int batch = p->batch, nb0 = batch / 2;
+    cudaStream_t main = p->stream;
+    CUDA_TRY(cudaEventRecord(p->fork_ev, main));
+    CUDA_TRY(cudaStreamWaitEvent(p->stream2, p->fork_ev, 0));
+    p->batch = nb0;
+    rc = record_passes(p, alg, iters, subset, flags, out);
+    if (!rc) {
+        p->stream = p->stream2;
+        p->view0 = nb0;
+        p->batch = batch - nb0;
+        rc = record_passes(p, alg, iters, subset, flags, out);
+    }
+    p->stream = main;
+    p->view0 = 0;
+    p->batch = batch;
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(p->join_ev, p->stream2));
+    CUDA_TRY(cudaStreamWaitEvent(main, p->join_ev, 0));
     return HS_OK;
 }
 
@@ -861,6 +904,9 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
     CUDA_TRY(cudaSetDevice(device));
     CUDA_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&p->fork_ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&p->join_ev, cudaEventDisableTiming));
     for (int k = 0; k < 2; ++k) {
         CUDA_TRY(cudaEventCreateWithFlags(&p->solved[k], cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&p->copied[k], cudaEventDisableTiming));
@@ -962,6 +1008,9 @@ void hs_plan_destroy(hs_plan *p)
     dfree(p->d_tiles);
     cudaStreamDestroy(p->stream);
     cudaStreamDestroy(p->copy_stream);
+    cudaStreamDestroy(p->stream2);
+    cudaEventDestroy(p->fork_ev);
+    cudaEventDestroy(p->join_ev);
     for (int k = 0; k < 2; ++k) {
         cudaEventDestroy(p->solved[k]);
         cudaEventDestroy(p->copied[k]);
@@ -1182,7 +1231,11 @@ static int solve_into(hs_plan *p, int alg, int iters, int64_t subset, const doub
     p->last_alg = alg;
     p->last_iters = iters;
     p->last_flags = flags;
-    p->last_launches = (alg == HS_ALG_RS) ? 2 : 2 + iters;  // tables(+seed) + passes
+    {   // tables(+seed) + passes, per graph branch
+        static const bool no_split = getenv("HS_SPLIT") && atoi(getenv("HS_SPLIT")) == 0;
+        const int branches = (p->batch >= kSplitBatch && !no_split) ? 2 : 1;
+        p->last_launches = 1 + (int64_t)branches * ((alg == HS_ALG_RS) ? 1 : iters + 1);
+    }
     return HS_OK;
 }
 

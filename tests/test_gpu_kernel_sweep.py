@@ -58,14 +58,15 @@ def test_multi_slab_window_lists():
 
 
 def test_batched_multi_slab_restaging_is_batch_invariant():
-    """1152^2, N = 100, B = 12: CTAs stream several chunks and re-stage their
-    gx slab when a chunk lies in the next slab; results equal solo solves
+    """1152^2, N = 100, B = 16: CTAs stream several chunks and re-stage their
+    gx slab when a chunk lies in the next slab, and the solve graph runs the
+    two halves of the batch as parallel branches; results equal solo solves
     bit for bit and the oracle within tolerance."""
     p = hs.build_pupil(1152)
-    sets = [hs.random_foci(100, 900 + k) for k in range(12)]
+    sets = [hs.random_foci(100, 900 + k) for k in range(16)]
     cfg = hs.SolverConfig("cswgs", iterations=5, compression=1 / 16, seed=0)
-    batch = hs.solve_batch(p, sets, cfg, seeds=list(range(12)))
-    for k in (0, 7, 11):
+    batch = hs.solve_batch(p, sets, cfg, seeds=list(range(16)))
+    for k in (0, 7, 8, 15):
         solo, _ = hs.solve(p, sets[k], hs.SolverConfig("cswgs", 5, 1 / 16, seed=k))
         assert np.array_equal(batch[k][0].phase, solo.phase)
     holo = batch[7][0]
