@@ -703,6 +703,8 @@ int launch_slab(hs_plan *p, int mode, const DevList &l, int32_t nunits, const Up
             }
         }
     }
+    static const int cpc_env = getenv("HS_SLAB_CPC") ? atoi(getenv("HS_SLAB_CPC")) : 0;
+    if (!half && cpc_env > 0 && cpc_env <= kGroup / 2 && (kGroup / 2) % cpc_env == 0) best = cpc_env;
     a.cpc = best;
     const dim3 grid(half ? (unsigned)(2 * span) : (unsigned)((span + best - 1) / best), p->batch);
     return launch_pass_kernel(p, hs_select_slab(c.ns, half), grid, dim3(half ? kSlabThreads / 2 : kSlabThreads),
