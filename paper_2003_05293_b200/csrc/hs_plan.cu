@@ -380,6 +380,18 @@ int build_slab_window(hs_plan *p, int64_t start, int64_t count, int np, DevList 
             e.y = 0;
             ent[base + idx] = e;
         }
+        // row hint: the second entry of every pair carries (in its row bits,
+        // which the kernel does not read for the column) the row of the
+        // stream's next run in the chunk, so the kernel prefetches that gy
+        // row a run ahead
+        for (size_t sbase = base; sbase < ent.size(); sbase += kSlabP) {
+            int hint = ent[sbase + kSlabP - 2].x >> 16;
+            for (int t = kSlabP - 2; t >= 0; t -= 2) {
+                const int row = ent[sbase + t].x >> 16;
+                ent[sbase + t + 1].x = (hint << 16) | (ent[sbase + t + 1].x & 0xffff);
+                if (t > 0 && (ent[sbase + t - 2].x >> 16) != row) hint = row;
+            }
+        }
         for (size_t q = base; q < ent.size(); q += kSlabL) c0s.push_back((int32_t)slab * sw);
     }
     int r;

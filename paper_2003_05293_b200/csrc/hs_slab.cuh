@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
     static_assert(GPW * WPC == kSlabStreams, "32 streams per chunk");
     extern __shared__ float4 sm4[];
     __shared__ __align__(8) unsigned long long bar;
+    __shared__ int s_next_c0;
 
     hs_pdl_launch_next();
     const int pat = blockIdx.y;
@@ -185,7 +186,8 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
     __syncthreads();
 
     const float2 *__restrict__ gx = a.gx + (int64_t)pat * a.tab_stride;
-    const float2 *__restrict__ Y = a.gy + (int64_t)pat * a.tab_stride + VEC * g;
+    const float2 *__restrict__ Yrow0 = a.gy + (int64_t)pat * a.tab_stride;
+    const float2 *__restrict__ Y = Yrow0 + VEC * g;
     uint32_t phase = 0;
     int c0 = -1;
 
@@ -315,6 +317,11 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
             if (rcur >= 0) flush();
             new_row(r);
             rcur = r;
+            // the second entry's row bits carry the row of this stream's next
+            // run: pull that gy row into L1 now, a run ahead of new_row
+            const int rn = e.z >> 16;
+            if (rn != r && g < NS + 1)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(Yrow0 + (int64_t)rn * NP + min(16 * g, NP - 1)));
         }
         // backward partials of both pixels over this lane's spots (FFMA2)
         f2x m0 = 0ull, m1 = 0ull, o0 = 0ull, o1 = 0ull;
@@ -393,7 +400,7 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
         store_ent(qi + 2);  // chunk qi's buffer is consumed
         __syncwarp();
         if (qi + 1 < nq) {
-            const int cs = __ldg(a.chunk_c0 + q0 + qi + 1);
+            const int cs = s_next_c0;  // read at the chunk's start
             if (cs != c0)
                 stage(cs);        // begins with __syncthreads
             else
@@ -403,6 +410,9 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
 
     for (int qi = 0; qi < nq; ++qi) {
         fetch_ent(qi + 2);
+        // the next chunk's slab origin, read now (the previous chunk's last
+        // barrier ordered the previous reads of s_next_c0 before this write)
+        if (tid == 0 && qi + 1 < nq) s_next_c0 = __ldg(a.chunk_c0 + q0 + qi + 1);
 #pragma unroll 1
         for (int t = 0; t < P; t += 16) {
 #pragma unroll
