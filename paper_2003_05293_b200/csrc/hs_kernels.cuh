@@ -109,6 +109,11 @@ __device__ __forceinline__ void hs_pdl_launch_next()
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+__device__ __forceinline__ uint32_t hs_smem_addr(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 __device__ __forceinline__ void hs_pdl_wait_prev()
 {
     asm volatile("griddepcontrol.wait;" ::: "memory");

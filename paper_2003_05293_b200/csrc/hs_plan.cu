@@ -26,6 +26,7 @@
 #include "hs_tilek.cuh"
 #include "hs_xchg.cuh"
 #include "hs_slab.cuh"
+#include "hs_umma.cuh"
 
 using namespace hs;
 
@@ -149,8 +150,11 @@ struct hs_plan {
     double *d_axis = nullptr;
     float *d_amp_img = nullptr;           // [side][side] amplitude, 0 outside
     int32_t *d_idx_img = nullptr;         // [side][side] storage index, -1 outside
-    int32_t *d_tiles = nullptr;           // non-empty 64x32 tiles, packed (r0 << 16) | c0
+    int32_t *d_tiles = nullptr;           // non-empty 64x64 tiles, packed (r0 << 16) | c0
     int32_t ntiles = 0;
+    int32_t *d_utiles = nullptr;          // non-empty 128x64 tiles of the tcgen05 full pass
+    int32_t nutiles = 0;
+    bool umma_enabled = true;             // HS_UMMA=0: FFMA tiles for every n
     int num_sms = 148;
     bool pdl = false;                     // next pass launch: programmatic dependent launch
     int view0 = 0;                        // first pattern of the sub-batch being recorded
@@ -644,16 +648,32 @@ int launch_pass_kernel(hs_plan *p, void (*fn)(Arg), dim3 grid, dim3 block, size_
     return HS_OK;
 }
 
-// Full-range fused pass with the GEMM-tile kernels (hs_tile: n <= 128, hs_tilek: larger n).
+// Full-range tile list of the current configuration: the tcgen05 pass's
+// 128 x 64 tiles when np <= 112 (hs_umma), else the FFMA 64 x 64 tiles.
+struct TileSet {
+    const int32_t *d;
+    int32_t n;
+    bool umma;
+};
+
+TileSet tile_set(const hs_plan *p)
+{
+    if (p->umma_enabled && p->cfg.ns > 0 && p->cfg.np <= kUNPMax) return {p->d_utiles, p->nutiles, true};
+    return {p->d_tiles, p->ntiles, false};
+}
+
+// Full-range fused pass: tcgen05 tiles (np <= 112), FFMA GEMM tiles (hs_tile:
+// n <= 128), spot-chunked FFMA tiles (hs_tilek: larger n).
 int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int32_t lo = 0, int32_t hi = -1,
                 unsigned char *raster = nullptr)
 {
-    if (hi < 0) hi = p->ntiles;
+    const TileSet ts = tile_set(p);
+    if (hi < 0) hi = ts.n;
     const Config &c = p->cfg;
-    if (p->ntiles > p->cap_chunks) return fail(HS_ECUDA, "fold buffers too small (%d tiles)", p->ntiles);
+    if (ts.n > p->cap_chunks) return fail(HS_ECUDA, "fold buffers too small (%d tiles)", ts.n);
     TileArgs a;
     memset(&a, 0, sizeof a);
-    a.tiles = p->d_tiles;
+    a.tiles = ts.d;
     a.side = p->side;
     a.np = c.np;
     a.tab_stride = (int64_t)p->side * c.np;
@@ -665,15 +685,17 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     a.phase_out = phase_out ? phase_out + (int64_t)p->view0 * p->m : nullptr;
     a.phase_stride = p->m;
     a.raster = raster ? raster + (int64_t)p->view0 * p->side * p->side : nullptr;
-    a.f = fold_args(p, p->ntiles, u, lo, hi);
+    a.f = fold_args(p, ts.n, u, lo, hi);
     a.n = p->n;
+    if (hi <= lo) return HS_OK;
+    dim3 grid(hi - lo, p->batch);
+    if (ts.umma)
+        return launch_pass_kernel(p, hs_select_umma(c.np, write), grid, dim3(kUThreads), hs_umma_smem_bytes(), a);
     const int spt = (p->n + 7) / 8;
     // n <= 128: all spots resident (hs_tile); larger n: spot-chunked (hs_tilek)
     const bool chunked = c.ns == 0;
     TileFn fn = chunked ? hs_select_tilek(write) : hs_select_tile(spt, write);
     const size_t smem = chunked ? hs_tilek_smem_bytes() : hs_tile_smem_bytes(spt, p->n);
-    if (hi <= lo) return HS_OK;
-    dim3 grid(hi - lo, p->batch);
     return launch_pass_kernel(p, fn, grid, dim3(kThreads), smem, a);
 }
 
@@ -968,12 +990,30 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
             for (int c0 = lo; c0 < hi; c0 += kTileC) tiles.push_back((r0 << 16) | c0);
         }
         p->ntiles = (int32_t)tiles.size();
+        // the tcgen05 pass: 128-row bands, same column rule
+        std::vector<int32_t> utiles;
+        for (int r0 = 0; r0 < side; r0 += kUR) {
+            int lo = side, hi = 0;
+            for (int r = r0; r < std::min(r0 + kUR, side); ++r) {
+                lo = std::min(lo, p->row_lo[r]);
+                hi = std::max(hi, p->row_hi[r]);
+            }
+            for (int c0 = lo; c0 < hi; c0 += kUC) utiles.push_back((r0 << 16) | c0);
+        }
+        p->nutiles = (int32_t)utiles.size();
         if ((rc = dalloc(&p->d_amp_img, cells)) || (rc = dalloc(&p->d_idx_img, cells)) ||
-            (rc = dalloc(&p->d_tiles, tiles.size())))
+            (rc = dalloc(&p->d_tiles, tiles.size())) || (rc = dalloc(&p->d_utiles, utiles.size())))
             return rc;
         CUDA_TRY(cudaMemcpy(p->d_amp_img, amp_img.data(), cells * sizeof(float), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(p->d_idx_img, p->h_index.data(), cells * sizeof(int32_t), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(p->d_utiles, utiles.data(), utiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        if (const char *env = getenv("HS_UMMA")) p->umma_enabled = atoi(env) != 0;
+        for (int np = 16; np <= kUNPMax; np += 16)
+            for (int w = 0; w < 2; ++w)
+                CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_umma(np, w != 0),
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)hs_umma_smem_bytes()));
         CUDA_TRY(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
         if (const char *env = getenv("HS_PDL")) p->pdl_enabled = atoi(env) != 0;
         for (int ns = 1; ns <= 8; ++ns)
@@ -1020,6 +1060,7 @@ void hs_plan_destroy(hs_plan *p)
     dfree(p->d_amp_img);
     dfree(p->d_idx_img);
     dfree(p->d_tiles);
+    dfree(p->d_utiles);
     cudaStreamDestroy(p->stream);
     cudaStreamDestroy(p->copy_stream);
     cudaStreamDestroy(p->stream2);
@@ -1052,7 +1093,7 @@ int hs_set_spots(hs_plan *p, int batch, int n, const double *x, const double *y,
         p->cfg.ns > 0 ? 2 * (p->m / kSlabL + p->side / hs_slab_width(p->cfg.np, p->side) + 2) : 0;
     const int64_t chunks = std::max<int64_t>({(int64_t)geom_of(*dense, dense->count, p->cfg.spw).nchunks,
                                               (int64_t)kTargetChunks + 1, p->m / kMaxChunk + 2,
-                                              (int64_t)p->ntiles, slab_chunks});
+                                              (int64_t)p->ntiles, (int64_t)p->nutiles, slab_chunks});
     if ((rc = ensure_fold(p, chunks))) return rc;
     const size_t bytes = sizeof(double) * (size_t)batch * n;
     CUDA_TRY(cudaMemcpyAsync(p->d_x, x, bytes, cudaMemcpyHostToDevice, p->stream));
@@ -1383,7 +1424,7 @@ static int shard_pass_desc(hs_plan *p, int j, int *kind, const DevList **list, i
     } else {
         *kind = 0;  // GEMM-tile full pass (every n)
         *list = nullptr;
-        *nchunks = p->ntiles;
+        *nchunks = tile_set(p).n;
         return HS_OK;
     }
     *list = lst;

@@ -78,11 +78,6 @@ __host__ __device__ constexpr size_t hs_slab_smem_bytes(int np, int sw)
     return sizeof(float2) * (size_t)np * sw + hs_slab_fixed_bytes(np);
 }
 
-__device__ __forceinline__ uint32_t hs_smem_addr(const void *p)
-{
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
 __device__ __forceinline__ float hs_rsqrt(float x)
 {
     float y;

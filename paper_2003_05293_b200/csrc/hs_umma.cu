@@ -1,0 +1,26 @@
+// Instantiates the tcgen05 full-range pass for np = 16 .. 112.
+#include "hs_umma.cuh"
+
+namespace hs {
+
+template <int NP>
+static UmmaFn pick(bool write)
+{
+    return write ? hs_umma_kernel<NP, true> : hs_umma_kernel<NP, false>;
+}
+
+UmmaFn hs_select_umma(int np, bool write)
+{
+    switch (np) {
+    case 16: return pick<16>(write);
+    case 32: return pick<32>(write);
+    case 48: return pick<48>(write);
+    case 64: return pick<64>(write);
+    case 80: return pick<80>(write);
+    case 96: return pick<96>(write);
+    case 112: return pick<112>(write);
+    default: return nullptr;
+    }
+}
+
+}  // namespace hs
