@@ -154,7 +154,7 @@ struct hs_plan {
     int32_t ntiles = 0;
     int32_t *d_utiles = nullptr;          // non-empty 128x64 tiles of the tcgen05 full pass
     int32_t nutiles = 0;
-    bool umma_enabled = true;             // HS_UMMA=0: FFMA tiles for every n
+    bool umma_enabled = false;            // HS_UMMA=1: tcgen05 full pass for np <= 112 (experimental)
     int num_sms = 148;
     bool pdl = false;                     // next pass launch: programmatic dependent launch
     int view0 = 0;                        // first pattern of the sub-batch being recorded

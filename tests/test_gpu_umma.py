@@ -1,0 +1,26 @@
+"""The tcgen05 full-range pass (csrc/hs_umma.cuh, HS_UMMA=1) under the same
+parity bar as the default FFMA tile pass: the solver cases of
+test_gpu_parity.py (golden runs, the grid100 quality gate, bitwise
+repeatability / batch invariance, c=1 == WGS) re-run in a child process with
+the tensor-core pass selected at plan creation.
+"""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def test_parity_with_tcgen05_full_pass():
+    env = dict(os.environ, HS_UMMA="1")
+    r = subprocess.run(
+        [sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+         os.path.join(HERE, "test_gpu_parity.py"),
+         "-k", "solver_matches or quality_gate or bitwise or wgs_equals or trace_weight or pipelined"],
+        env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
