@@ -175,6 +175,8 @@ struct hs_plan {
     double *d_x = nullptr, *d_y = nullptr, *d_z = nullptr, *d_a0 = nullptr;
     double *d_theta = nullptr, *d_amp_in = nullptr;
     float2 *d_gx = nullptr, *d_gy = nullptr;
+    float *d_gyp = nullptr;               // gy operand planes of the tcgen05 pass (umma_enabled)
+    int64_t gyp_stride = 0;
     double *d_w = nullptr;
     float2 *d_coef = nullptr;
     float2 *d_part = nullptr;
@@ -491,6 +493,7 @@ void free_batch(hs_plan *p)
     dfree(p->d_x); dfree(p->d_y); dfree(p->d_z); dfree(p->d_a0);
     dfree(p->d_theta); dfree(p->d_amp_in);
     dfree(p->d_gx); p->d_gy = nullptr; dfree(p->d_w); dfree(p->d_coef);
+    dfree(p->d_gyp); p->gyp_stride = 0;
     dfree(p->d_status); dfree(p->d_degen); dfree(p->d_qstatus);
     dfree(p->d_fields); dfree(p->d_e); dfree(p->d_u); dfree(p->d_inten); dfree(p->d_rel);
     dfree(p->d_out[1]);
@@ -522,6 +525,13 @@ int ensure_batch(hs_plan *p, int batch, int n)
         (rc = dalloc(&p->d_raster, (size_t)B * p->side * p->side))) {
         free_batch(p);
         return rc;
+    }
+    if (p->umma_enabled && cfg.ns > 0 && cfg.np <= kUNPMax) {
+        p->gyp_stride = hs_umma_plane_floats(p->side, cfg.np);
+        if ((rc = dalloc(&p->d_gyp, (size_t)B * p->gyp_stride))) {
+            free_batch(p);
+            return rc;
+        }
     }
     CUDA_TRY(cudaMemset(p->d_status, 0, sizeof(int32_t) * B));
     p->d_gy = p->d_gx + (size_t)B * p->side * cfg.np;  // one allocation: gx | gy
@@ -593,6 +603,22 @@ UpdArgs upd_args(hs_plan *p, int act)
     return u;
 }
 
+// Full-range tile list of the current configuration: the tcgen05 pass's
+// 128 x 64 tiles when np <= 112 (hs_umma), else the FFMA 64 x 64 tiles.
+struct TileSet {
+    const int32_t *d;
+    int32_t n;
+    bool umma;
+};
+
+TileSet tile_set(const hs_plan *p)
+{
+    if (p->umma_enabled && p->cfg.ns > 0 && p->cfg.np <= kUNPMax && p->d_gyp &&
+        p->gyp_stride >= hs_umma_plane_floats(p->side, p->cfg.np))
+        return {p->d_utiles, p->nutiles, true};
+    return {p->d_tiles, p->ntiles, false};
+}
+
 int launch_tables(hs_plan *p, bool seed)
 {
     dim3 grid(p->side, p->batch);
@@ -600,6 +626,12 @@ int launch_tables(hs_plan *p, bool seed)
                                                   p->d_y, p->d_z, p->d_gx, p->d_gy, p->d_a0,
                                                   seed ? p->d_theta : nullptr, p->d_coef, p->d_w);
     CUDA_TRY(cudaGetLastError());
+    if (p->d_gyp && tile_set(p).umma) {
+        dim3 pg((unsigned)((p->side + kUR - 1) / kUR * (p->cfg.np / kUF)), p->batch);
+        hs_umma_prep_kernel<<<pg, 256, 0, p->stream>>>(p->d_gy, p->d_gyp, p->side, p->cfg.np,
+                                                       (int64_t)p->side * p->cfg.np, p->gyp_stride);
+        CUDA_TRY(cudaGetLastError());
+    }
     return HS_OK;
 }
 
@@ -648,19 +680,6 @@ int launch_pass_kernel(hs_plan *p, void (*fn)(Arg), dim3 grid, dim3 block, size_
     return HS_OK;
 }
 
-// Full-range tile list of the current configuration: the tcgen05 pass's
-// 128 x 64 tiles when np <= 112 (hs_umma), else the FFMA 64 x 64 tiles.
-struct TileSet {
-    const int32_t *d;
-    int32_t n;
-    bool umma;
-};
-
-TileSet tile_set(const hs_plan *p)
-{
-    if (p->umma_enabled && p->cfg.ns > 0 && p->cfg.np <= kUNPMax) return {p->d_utiles, p->nutiles, true};
-    return {p->d_tiles, p->ntiles, false};
-}
 
 // Full-range fused pass: tcgen05 tiles (np <= 112), FFMA GEMM tiles (hs_tile:
 // n <= 128), spot-chunked FFMA tiles (hs_tilek: larger n).
@@ -674,6 +693,8 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     TileArgs a;
     memset(&a, 0, sizeof a);
     a.tiles = ts.d;
+    a.gyp = p->d_gyp ? p->d_gyp + p->view0 * p->gyp_stride : nullptr;
+    a.gyp_stride = p->gyp_stride;
     a.side = p->side;
     a.np = c.np;
     a.tab_stride = (int64_t)p->side * c.np;
@@ -998,7 +1019,7 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
                 lo = std::min(lo, p->row_lo[r]);
                 hi = std::max(hi, p->row_hi[r]);
             }
-            for (int c0 = lo; c0 < hi; c0 += kUC) utiles.push_back((r0 << 16) | c0);
+            for (int c0 = lo & ~3; c0 < hi; c0 += kUC) utiles.push_back((r0 << 16) | c0);  // 16-B aligned amp rows
         }
         p->nutiles = (int32_t)utiles.size();
         if ((rc = dalloc(&p->d_amp_img, cells)) || (rc = dalloc(&p->d_idx_img, cells)) ||

@@ -39,6 +39,8 @@ struct TileArgs {
     int32_t n;                // real spots
     int64_t tab_stride;       // side * np
     const float2 *gx, *gy;    // [B][side][np]
+    const float *gyp;         // [B][gyp_stride] gy operand planes of the tcgen05 pass (hs_umma.cuh)
+    int64_t gyp_stride;
     const float2 *coef;       // [B][np]
     const float *amp_img;     // [side][side], 0 outside the aperture
     const int32_t *idx_img;   // [side][side] storage index, -1 outside

@@ -6,6 +6,7 @@ the tensor-core pass selected at plan creation.
 """
 
 import os
+import re
 import subprocess
 import sys
 
@@ -24,3 +25,5 @@ def test_parity_with_tcgen05_full_pass():
          "-k", "solver_matches or quality_gate or bitwise or wgs_equals or trace_weight or pipelined"],
         env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    m = re.search(r"(\d+) passed", r.stdout)
+    assert m and int(m.group(1)) >= 12, r.stdout[-2000:]

@@ -1,3 +1,7 @@
 mkdir -p gpurun_out
-HS_UMMA=1 timeout 600 ncu --set full --import-source on --clock-control none -k regex:hs_umma -s 2 -c 1 -o gpurun_out/umma32 python tools/profile_pass.py --which 0 --batch 32 --reps 1 > gpurun_out/ncu_umma.log 2>&1
-tail -3 gpurun_out/ncu_umma.log
+rm -f gpurun_out/pp.txt
+HS_UMMA=1 timeout 300 python tools/profile_pass.py --which 0 --batch 32 --reps 20 >> gpurun_out/pp.txt 2>&1
+HS_UMMA=1 timeout 300 python tools/profile_pass.py --which 0 --batch 1 --reps 20 >> gpurun_out/pp.txt 2>&1
+tail -5 gpurun_out/pp.txt
+timeout 900 python -m pytest tests/test_gpu_umma.py -x -q > gpurun_out/pytest_umma.txt 2>&1
+tail -30 gpurun_out/pytest_umma.txt
