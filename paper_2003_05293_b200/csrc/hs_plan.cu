@@ -154,7 +154,7 @@ struct hs_plan {
     int32_t ntiles = 0;
     int32_t *d_utiles = nullptr;          // non-empty 128x64 tiles of the tcgen05 full pass
     int32_t nutiles = 0;
-    bool umma_enabled = false;            // HS_UMMA=1: tcgen05 full pass for np <= 112 (experimental)
+    bool umma_enabled = true;             // HS_UMMA=0: FFMA tiles (hs_tile) for every n
     int num_sms = 148;
     bool pdl = false;                     // next pass launch: programmatic dependent launch
     int view0 = 0;                        // first pattern of the sub-batch being recorded
@@ -627,8 +627,8 @@ int launch_tables(hs_plan *p, bool seed)
                                                   seed ? p->d_theta : nullptr, p->d_coef, p->d_w);
     CUDA_TRY(cudaGetLastError());
     if (p->d_gyp && tile_set(p).umma) {
-        dim3 pg((unsigned)((p->side + kUR - 1) / kUR * (p->cfg.np / kUF)), p->batch);
-        hs_umma_prep_kernel<<<pg, 256, 0, p->stream>>>(p->d_gy, p->d_gyp, p->side, p->cfg.np,
+        dim3 pg((unsigned)((p->side + kUR - 1) / kUR * (p->cfg.np / kUF) + hs_umma_xblocks(p->side)), p->batch);
+        hs_umma_prep_kernel<<<pg, 256, 0, p->stream>>>(p->d_gx, p->d_gy, p->d_gyp, p->side, p->cfg.np,
                                                        (int64_t)p->side * p->cfg.np, p->gyp_stride);
         CUDA_TRY(cudaGetLastError());
     }
@@ -1019,7 +1019,7 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
                 lo = std::min(lo, p->row_lo[r]);
                 hi = std::max(hi, p->row_hi[r]);
             }
-            for (int c0 = lo & ~3; c0 < hi; c0 += kUC) utiles.push_back((r0 << 16) | c0);  // 16-B aligned amp rows
+            for (int c0 = lo & ~7; c0 < hi; c0 += kUC) utiles.push_back((r0 << 16) | c0);  // X^T plane blocks of 8
         }
         p->nutiles = (int32_t)utiles.size();
         if ((rc = dalloc(&p->d_amp_img, cells)) || (rc = dalloc(&p->d_idx_img, cells)) ||

@@ -22,19 +22,25 @@
 //   TMEM [0, 128)     S = {Sr, Si} x 64 columns                            backward
 //        [0, 2 NP)    T = {Tr, Ti} x NP spots                              forward
 // S is read once into registers (b: 32 columns per thread), which frees the
-// columns T reuses.  The backward's A operand gy is constant for the whole
-// solve: hs_umma_prep_kernel writes its tf32 hi/lo planes once per table
-// build, already in the shared-memory operand layout, and each k-step's
-// 16 KB block is one TMA bulk copy (issued one chunk ahead); the per-pass
-// coefficients go on the B side (coef_k gx[c][k], built by the threads).
-// The same planes give the E epilogue coalesced gy reads (hi + lo == gy
-// exactly).  Shared memory: a ring of three operand stages, each either a
-// backward k-step (gy: 128 rows x 8 spots, X: 64 columns x 8 spots) or a
-// forward k-step (b': 128 rows x 8 columns, X^T: NP spots x 8 columns), 4
-// planes each, in the SWIZZLE_NONE K-major canonical layout (8 x 16-byte
-// core matrices).  One thread issues the MMAs and commits each stage to its
-// mbarrier; the threads wait for the MMAs two stages back before reusing a
-// stage, so the tensor pipe always has the previous k-step queued.
+// columns T reuses.  The operands that do not change between passes are
+// written once per table build by hs_umma_prep_kernel as tf32 hi/lo planes
+// already in the shared-memory operand layout -- gy (A of the backward,
+// [band][k-step] blocks of 16 KB) and X^T (B of the forward, 8-column blocks
+// of 14 KB) -- and each k-step's block is one TMA bulk copy; the per-pass
+// coefficients go on the B side of the backward (X' = coef_k gx[c][k],
+// built by warps 4-7) and b' (A of the forward) is written by every thread
+// for its row.  The gy planes also give the E epilogue coalesced gy reads
+// (hi + lo == gy exactly).  Shared memory: an A ring of 4 x 16 KB and a B
+// ring of 3 x 14 KB, SWIZZLE_NONE K-major canonical layout (8 x 16-byte core
+// matrices).  Per k-step every thread arrives on an operand mbarrier after
+// writing its part (no CTA-wide barrier); thread 0 waits for it and for the
+// TMA, issues the 12 MMAs and commits them to the step's MMA-done barrier;
+// the threads wait for the MMAs two steps back before reusing a slot.
+//
+// What bounds it (ncu, B = 16): the tensor pipe is ~45% active; each
+// 128 x 64 x 8 tf32 MMA reads 6 KB of operands from shared memory, so the
+// 12-MMA complex k-step is close to shared-memory-bandwidth bound; the
+// remainder is the per-tile CUDA-core work (b, E reduce, fold).
 //
 // Encodings (instruction descriptor, shared-memory descriptor, TMEM
 // st / ld, a_negate) are checked by tools/umma_probe.cu.
@@ -51,49 +57,77 @@ constexpr int kUF = 8;           // spots / columns per stage (one MMA k-step)
 constexpr int kUNPMax = 112;     // largest np (TMEM: 2 np <= 256)
 constexpr int kUThreads = 256;
 constexpr int kUTmem = 256;      // TMEM columns per CTA (two CTAs per SM)
-constexpr int kUStages = 3;
+constexpr int kUA = 4;           // A ring: gy planes (backward, TMA) / b' (forward, threads)
+constexpr int kUB = 3;           // B ring: X' (backward, threads) / X^T planes (forward, TMA)
 constexpr int kUAPl = kUR * kUF * 4;                // A plane [128][8] (4 KB)
-constexpr int kUBOff = 4 * kUAPl;                   // B planes after the 4 A planes
-constexpr int kUSlot = kUBOff + 4 * kUNPMax * kUF * 4;  // 30 KB: b' + X^T at np = 112
-constexpr int kUPlaneBlock = 4 * kUAPl;             // gy planes of one (band, k-step): 16 KB
+constexpr int kUASlot = 4 * kUAPl;                  // 16 KB
+constexpr int kUBSlot = 4 * kUNPMax * kUF * 4;      // 14 KB: X^T at np = 112 (X' needs 8 KB)
 
 __host__ __device__ constexpr size_t hs_umma_smem_bytes()
 {
-    // operand stages + 1 KB alignment + E reduce scratch [8 warps][64] float
-    return kUStages * (size_t)kUSlot + 1024 + 8 * 64 * sizeof(float);
+    // rings + 128 B alignment slack + E reduce scratch [8 warps][32] float
+    return (size_t)kUA * kUASlot + (size_t)kUB * kUBSlot + 128 + 8 * 32 * sizeof(float);
 }
 
-// gy planes of one pattern: [band][k-step][4][128 rows][8 spots] floats
+// Operand planes of one pattern (constant per table build):
+//   gy : [band][k-step][4][128 rows][8 spots]       (A of the backward)
+//   X^T: [column block of 8][4][np spots][8 columns] (B of the forward),
+//        ceil(side / 8) + 8 blocks (the tail blocks are zero)
+__host__ __device__ constexpr int64_t hs_umma_gy_floats(int side, int np)
+{
+    return (int64_t)((side + kUR - 1) / kUR) * (np / kUF) * (kUASlot / 4);
+}
+__host__ __device__ constexpr int hs_umma_xblocks(int side) { return (side + 7) / 8 + 8; }
 __host__ __device__ constexpr int64_t hs_umma_plane_floats(int side, int np)
 {
-    return (int64_t)((side + kUR - 1) / kUR) * (np / kUF) * (kUPlaneBlock / 4);
+    return hs_umma_gy_floats(side, np) + (int64_t)hs_umma_xblocks(side) * 4 * np * kUF;
 }
 
 // Offset (floats) of element (r, k) in a [128][8] K-major operand plane.
 __host__ __device__ constexpr int hs_uoff(int r, int k) { return r * 4 + (k >> 2) * 512 + (k & 3); }
 
-// gy -> tf32 hi/lo planes {re_h, re_l, im_h, im_l} in the operand layout.
-// grid (bands * np / 8, B), 256 threads.
-static __global__ void hs_umma_prep_kernel(const float2 *__restrict__ gy, float *__restrict__ planes, int side,
-                                           int np, int64_t tab_stride, int64_t plane_stride)
+__device__ __forceinline__ void hs_split_store(float v, float *dst, int plane_floats)
+{
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
+    dst[0] = __uint_as_float(h);
+    dst[plane_floats] = v - __uint_as_float(h);
+}
+
+// gy / gx -> tf32 hi/lo planes {re_h, re_l, im_h, im_l} in the operand
+// layouts.  grid (bands * np / 8 + xblocks, B), 256 threads.
+static __global__ void hs_umma_prep_kernel(const float2 *__restrict__ gx, const float2 *__restrict__ gy,
+                                           float *__restrict__ planes, int side, int np, int64_t tab_stride,
+                                           int64_t plane_stride)
 {
     const int nks = np / kUF;
-    const int band = blockIdx.x / nks, ks = blockIdx.x % nks;
+    const int ngy = (side + kUR - 1) / kUR * nks;
     const int pat = blockIdx.y;
-    float *dst = planes + (int64_t)pat * plane_stride + (int64_t)blockIdx.x * (kUPlaneBlock / 4);
-    for (int i = threadIdx.x; i < kUR * kUF; i += blockDim.x) {
-        const int r = i / kUF, k = i % kUF;
-        const int grow = band * kUR + r;
-        float2 v = make_float2(0.f, 0.f);
-        if (grow < side) v = gy[(int64_t)pat * tab_stride + (int64_t)grow * np + ks * kUF + k];
-        uint32_t hr, hi;
-        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hr) : "f"(v.x));
-        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(v.y));
-        const int o = hs_uoff(r, k);
-        dst[o] = __uint_as_float(hr);
-        dst[o + kUAPl / 4] = v.x - __uint_as_float(hr);
-        dst[o + 2 * kUAPl / 4] = __uint_as_float(hi);
-        dst[o + 3 * kUAPl / 4] = v.y - __uint_as_float(hi);
+    float *base = planes + (int64_t)pat * plane_stride;
+    if ((int)blockIdx.x < ngy) {
+        const int band = blockIdx.x / nks, ks = blockIdx.x % nks;
+        float *dst = base + (int64_t)blockIdx.x * (kUASlot / 4);
+        for (int i = threadIdx.x; i < kUR * kUF; i += blockDim.x) {
+            const int r = i / kUF, k = i % kUF;
+            const int grow = band * kUR + r;
+            const float2 v = grow < side ? gy[(int64_t)pat * tab_stride + (int64_t)grow * np + ks * kUF + k]
+                                         : make_float2(0.f, 0.f);
+            const int o = hs_uoff(r, k);
+            hs_split_store(v.x, dst + o, kUAPl / 4);
+            hs_split_store(v.y, dst + o + kUAPl / 2, kUAPl / 4);
+        }
+    } else {
+        const int cb = blockIdx.x - ngy;
+        const int pl = np * kUF;  // plane floats
+        float *dst = base + hs_umma_gy_floats(side, np) + (int64_t)cb * 4 * pl;
+        for (int i = threadIdx.x; i < np * kUF; i += blockDim.x) {
+            const int k = i / kUF, c = i % kUF;
+            const int gc = cb * kUF + c;
+            const float2 v = gc < side ? gx[(int64_t)pat * tab_stride + (int64_t)gc * np + k] : make_float2(0.f, 0.f);
+            const int o = (k >> 3) * 32 + (c >> 2) * (np / 8) * 32 + (k & 7) * 4 + (c & 3);
+            hs_split_store(v.x, dst + o, pl);
+            hs_split_store(v.y, dst + o + 2 * pl, pl);
+        }
     }
 }
 
@@ -208,12 +242,14 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
 {
     static_assert(NP % 16 == 0 && NP <= kUNPMax, "forward N = np must be a multiple of 16, <= 112");
     constexpr int NCC = kUC / kUF;           // forward k-steps (8)
-    constexpr uint32_t BPL = kUC * kUF * 4;  // backward X plane bytes (2 KB)
+    constexpr uint32_t BPL = kUC * kUF * 4;  // backward X' plane bytes (2 KB)
     constexpr uint32_t FPL = NP * kUF * 4;   // forward X^T plane bytes
     constexpr uint32_t FLBO = (NP / 8) * 128;
     constexpr int KH = NP / 2;               // spots per thread in the E epilogue
-    extern __shared__ __align__(1024) unsigned char smu[];
-    __shared__ __align__(8) unsigned long long mbar[2 * kUStages];  // [0, 3) MMA done, [3, 6) TMA full
+    extern __shared__ __align__(128) unsigned char smu[];
+    // MMA done [0, 4), A full (gy TMA) [4, 8), B full (X^T TMA) [8, 11),
+    // operands written (all threads arrive) [11, 15)
+    __shared__ __align__(8) unsigned long long mbar[3 * kUA + kUB];
     __shared__ uint32_t s_tmem;
     __shared__ float2 coef_s[NP];
 
@@ -224,33 +260,38 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
     const int q = warp & 3, h = warp >> 2;  // TMEM lane quarter, column / spot half
     const int row = 32 * q + lane;          // tile row of this thread (TMEM lane)
     const int packed = __ldg(a.tiles + tile);
-    const int r0 = packed >> 16, c0 = packed & 0xffff;
+    const int r0 = packed >> 16, c0 = packed & 0xffff;  // c0: multiple of 8
     const float2 *gx = a.gx + (int64_t)pat * a.tab_stride;
-    const float *gyp = a.gyp + (int64_t)pat * a.gyp_stride + (int64_t)(r0 / kUR) * (NP / kUF) * (kUPlaneBlock / 4);
+    const float *pbase = a.gyp + (int64_t)pat * a.gyp_stride;
+    const float *gyp = pbase + (int64_t)(r0 / kUR) * (NP / kUF) * (kUASlot / 4);
+    const float *xtp = pbase + hs_umma_gy_floats(a.side, NP) + (int64_t)(c0 / kUF) * (4 * NP * kUF);
     const int n = a.n;
     const int ksteps = (n + 7) / 8;          // backward k-steps (8 spots)
-    const int nsteps = ksteps + NCC;         // stage sequence: backward, then forward
+    const int nsteps = ksteps + NCC;         // step sequence: backward, then forward
 
-    unsigned char *sbase = reinterpret_cast<unsigned char *>(((uintptr_t)smu + 1023) & ~(uintptr_t)1023);
+    unsigned char *sbase = reinterpret_cast<unsigned char *>(((uintptr_t)smu + 127) & ~(uintptr_t)127);
     const uint32_t sb = hs_smem_addr(sbase);
-    float *red = reinterpret_cast<float *>(sbase + kUStages * kUSlot);  // [8][64]
+    const uint32_t sa = sb, sbb = sb + kUA * kUASlot;  // A ring, B ring
+    float *red = reinterpret_cast<float *>(sbase + kUA * kUASlot + kUB * kUBSlot);  // [8][32]
     const int grow = r0 + row;
     const bool row_in = grow < a.side;
 
-    // ---- backward X loads: thread (column c = tid / 2, spot quad kq = tid % 2)
-    // of threads < 128 loads spots 8 ks + 4 kq .. + 4 of gx[c0 + c]
-    const bool xb_on = tid < 2 * kUC;
+    // ---- backward X' loads: thread (column c = tid / 2, spot quad kq = tid % 2)
+    // of threads < 128 loads spots 8 ks + 4 kq .. + 4 of gx[c0 + c]; two
+    // k-steps in flight
+    const bool xb_on = tid >= kUThreads - 2 * kUC;  // warps 4-7 (warp 0 issues the MMAs)
     const int xb_c = (tid >> 1) & (kUC - 1), xb_kq = tid & 1;
     const float4 *xb_src = reinterpret_cast<const float4 *>(gx + (int64_t)min(c0 + xb_c, a.side - 1) * a.np);
-    float4 xb0 = make_float4(0.f, 0.f, 0.f, 0.f), xb1 = xb0;
-    auto load_b = [&](int ks) {
-        const int k = ks * kUF + 4 * xb_kq;
-        if (xb_on) {
-            xb0 = __ldg(xb_src + k / 2);
-            xb1 = __ldg(xb_src + k / 2 + 1);
+    float4 xq[2], xn[2];  // k-step ks, ks + 1
+    auto load_b = [&](int ks, float4 (&d)[2]) {
+        if (xb_on && ks < ksteps) {
+            const int k = ks * kUF + 4 * xb_kq;
+            d[0] = __ldg(xb_src + k / 2);
+            d[1] = __ldg(xb_src + k / 2 + 1);
         }
     };
-    load_b(0);  // gx: an input of the whole solve
+    load_b(0, xq);  // gx: an input of the whole solve
+    load_b(1, xn);
 
     // -- below: the previous pass's results (status, coef); TMEM is taken
     // only now, so a dependent-launched CTA never holds it while waiting
@@ -262,20 +303,37 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
                      "n"(kUTmem));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    const uint32_t bar = hs_smem_addr(&mbar[0]);  // stage s: MMA done bar + 8 s, TMA full bar + 8 (3 + s)
-    auto tma_gy = [&](int ks) {  // gy planes of k-step ks -> stage ks % 3 (thread 0)
-        const int s = ks % kUStages;
-        const uint32_t fb = bar + 8 * (kUStages + s);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "n"(kUPlaneBlock) : "memory");
+    const uint32_t bar = hs_smem_addr(&mbar[0]);
+    const uint32_t bar_af = bar + 8 * kUA, bar_bf = bar + 16 * kUA, bar_op = bar + 8 * (2 * kUA + kUB);
+    auto bulk = [](uint32_t dst, const float *src, uint32_t bytes, uint32_t fb) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         sb + s * kUSlot),
-                     "l"(gyp + (int64_t)ks * (kUPlaneBlock / 4)), "n"(kUPlaneBlock), "r"(fb)
+                         dst),
+                     "l"(src), "r"(bytes), "r"(fb)
                      : "memory");
     };
+    // (thread 0) gy planes of backward step j -> A slot j % 4, two steps
+    // ahead (slot last used by j - 4); X^T planes of forward step j -> B slot
+    // j % 3, one step ahead (slot last used by j - 3).  Issued at step i after
+    // the wait for MMA(i - 2).
+    auto tma_ahead = [&](int i) {
+        if (i + 2 < ksteps) {
+            const int j = i + 2;
+            bulk(sa + (j % kUA) * kUASlot, gyp + (int64_t)j * (kUASlot / 4), kUASlot, bar_af + 8 * (j % kUA));
+        }
+        if (i + 1 >= ksteps && i + 1 < nsteps) {
+            const int j = i + 1;
+            bulk(sbb + (j % kUB) * kUBSlot, xtp + (int64_t)(j - ksteps) * (4 * NP * kUF), 4 * FPL,
+                 bar_bf + 8 * (j % kUB));
+        }
+    };
     if (tid == 0) {
-        for (int i = 0; i < 2 * kUStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar + 8 * i));
+        for (int i = 0; i < 2 * kUA + kUB; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar + 8 * i));
+        for (int i = 0; i < kUA; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_op + 8 * i), "n"(kUThreads));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        tma_gy(0);
+        bulk(sa, gyp, kUASlot, bar_af);  // step 0; step 1 (gy or X^T) by tma_ahead(-1)
+        tma_ahead(-1);
     }
     hs_tc_fence_before();
     __syncthreads();
@@ -283,80 +341,91 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
     const uint32_t tm = s_tmem;
     const uint32_t tl = tm + ((uint32_t)(32 * q) << 16);  // this warp's lane quarter
 
-    // MMA completion of stage-sequence step j is completion (j / 3) of
-    // barrier j % 3; waits happen in order, never two phases behind.
+    // MMA completion of step j is completion (j / 4) of barrier j % 4; waits
+    // happen in order, never two phases behind.
     int done = 0;  // steps known complete
     auto wait_mma = [&](int j) {
-        for (; done <= j; ++done) hs_mbar_wait(bar + 8 * (done % kUStages), (uint32_t)(done / kUStages) & 1u);
+        for (; done <= j; ++done) hs_mbar_wait(bar + 8 * (done % kUA), (uint32_t)(done / kUA) & 1u);
         hs_tc_fence_after();
+    };
+    // TMA completions (thread 0 only): in step order per slot
+    uint32_t af_ph = 0, bf_ph = 0;  // parity bit per slot
+    auto wait_tma = [&](int j) {
+        if (j < ksteps) {
+            const int s = j % kUA;
+            hs_mbar_wait(bar_af + 8 * s, (af_ph >> s) & 1u);
+            af_ph ^= 1u << s;
+        } else {
+            const int s = j % kUB;
+            hs_mbar_wait(bar_bf + 8 * s, (bf_ph >> s) & 1u);
+            bf_ph ^= 1u << s;
+        }
     };
     auto commit = [&](int j) {  // thread 0, after issuing step j's MMAs
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         bar + 8 * (j % kUStages))
+                         bar + 8 * (j % kUA))
                      : "memory");
     };
-    // operands written by the threads (generic proxy) become visible to the
-    // MMA-issuing thread (async proxy)
-    auto publish = [&]() {
+    // Step j's operands written by the threads (generic proxy; TMEM reads
+    // retired) become visible to the MMA-issuing thread (async proxy): every
+    // thread arrives on operand barrier j % 4 (completion j / 4), thread 0
+    // waits for it.  No CTA-wide barrier per step: the other warps run ahead
+    // until the MMA-done wait two steps back.
+    auto publish = [&](int j) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         hs_tc_fence_before();
-        __syncthreads();
-        hs_tc_fence_after();
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_op + 8 * (j % kUA)) : "memory");
+        if (tid == 0) {
+            hs_mbar_wait(bar_op + 8 * (j % kUA), (uint32_t)(j / kUA) & 1u);
+            hs_tc_fence_after();
+        }
     };
     auto mma_ss = [](uint32_t d, uint64_t av, uint64_t bv, uint32_t id, uint32_t acc) { hs_mma_ss(d, av, bv, id, acc); };
+    // step j's MMAs (thread 0): A slot j % 4 (LBO 2048, SBO 128), B slot j % 3
+    auto issue = [&](int j, uint32_t dr, uint32_t di, uint32_t lbo, uint32_t bpl, uint32_t id, uint32_t idn,
+                     uint32_t acc) {
+        const uint32_t as = sa + (j % kUA) * kUASlot, bs = sbb + (j % kUB) * kUBSlot;
+        const uint64_t xb[4] = {hs_sdesc(bs, lbo, 128), hs_sdesc(bs + bpl, lbo, 128), hs_sdesc(bs + 2 * bpl, lbo, 128),
+                                hs_sdesc(bs + 3 * bpl, lbo, 128)};
+        hs_cmma(mma_ss, dr, di, [&](int pl) { return hs_sdesc(as + pl * kUAPl, 2048, 128); }, xb, id, idn, acc);
+        commit(j);
+    };
 
     // ---- backward: S = gy (coef X)^T ------------------------------------------
     const uint32_t idb = hs_idesc_tf32(kUC, false), idbn = hs_idesc_tf32(kUC, true);
     for (int ks = 0; ks < ksteps; ++ks) {
-        const int s = ks % kUStages;
-        if (ks >= 2) wait_mma(ks - 2);  // stage of ks + 1 (and of ks) free
-        if (tid == 0 && ks + 1 < ksteps) tma_gy(ks + 1);
+        if (ks >= 2) wait_mma(ks - 2);  // A slot of ks + 2, B slots of ks + 1 and ks free
+        if (tid == 0) tma_ahead(ks);
         if (xb_on) {  // X' = coef_k gx[c][k], planes [64 columns][8 spots]: (c/8)*128 + (k/4)*1024 + (c%8)*16
             const int k = ks * kUF + 4 * xb_kq;
             const float2 w0 = coef_s[k], w1 = coef_s[k + 1], w2 = coef_s[k + 2], w3 = coef_s[k + 3];
-            const float xr0 = fmaf(w0.x, xb0.x, -w0.y * xb0.y), xi0 = fmaf(w0.x, xb0.y, w0.y * xb0.x);
-            const float xr1 = fmaf(w1.x, xb0.z, -w1.y * xb0.w), xi1 = fmaf(w1.x, xb0.w, w1.y * xb0.z);
-            const float xr2 = fmaf(w2.x, xb1.x, -w2.y * xb1.y), xi2 = fmaf(w2.x, xb1.y, w2.y * xb1.x);
-            const float xr3 = fmaf(w3.x, xb1.z, -w3.y * xb1.w), xi3 = fmaf(w3.x, xb1.w, w3.y * xb1.z);
+            const float4 u0 = xq[0], u1 = xq[1];
+            const float xr0 = fmaf(w0.x, u0.x, -w0.y * u0.y), xi0 = fmaf(w0.x, u0.y, w0.y * u0.x);
+            const float xr1 = fmaf(w1.x, u0.z, -w1.y * u0.w), xi1 = fmaf(w1.x, u0.w, w1.y * u0.z);
+            const float xr2 = fmaf(w2.x, u1.x, -w2.y * u1.y), xi2 = fmaf(w2.x, u1.y, w2.y * u1.x);
+            const float xr3 = fmaf(w3.x, u1.z, -w3.y * u1.w), xi3 = fmaf(w3.x, u1.w, w3.y * u1.z);
             float4 rh, rl, ih, il;
             hs_split4(xr0, xr1, xr2, xr3, rh, rl);
             hs_split4(xi0, xi1, xi2, xi3, ih, il);
-            unsigned char *d = sbase + s * kUSlot + kUBOff + (xb_c >> 3) * 128 + xb_kq * 1024 + (xb_c & 7) * 16;
+            unsigned char *d = sbase + kUA * kUASlot + (ks % kUB) * kUBSlot + (xb_c >> 3) * 128 + xb_kq * 1024 +
+                               (xb_c & 7) * 16;
             *reinterpret_cast<float4 *>(d) = rh;
             *reinterpret_cast<float4 *>(d + BPL) = rl;
             *reinterpret_cast<float4 *>(d + 2 * BPL) = ih;
             *reinterpret_cast<float4 *>(d + 3 * BPL) = il;
         }
-        if (ks + 1 < ksteps) load_b(ks + 1);  // next k-step's loads in flight across the publish
-        publish();
+        xq[0] = xn[0];
+        xq[1] = xn[1];
+        load_b(ks + 2, xn);  // two k-steps in flight
+        publish(ks);
         if (tid == 0) {
-            hs_mbar_wait(bar + 8 * (kUStages + s), (uint32_t)(ks / kUStages) & 1u);  // gy planes landed
-            const uint32_t xs = sb + s * kUSlot;
-            const uint64_t xb[4] = {hs_sdesc(xs + kUBOff, 1024, 128), hs_sdesc(xs + kUBOff + BPL, 1024, 128),
-                                    hs_sdesc(xs + kUBOff + 2 * BPL, 1024, 128),
-                                    hs_sdesc(xs + kUBOff + 3 * BPL, 1024, 128)};
-            hs_cmma(mma_ss, tm, tm + kUC, [&](int pl) { return hs_sdesc(xs + pl * kUAPl, 2048, 128); }, xb, idb,
-                    idbn, ks ? 1u : 0u);
-            commit(ks);
+            wait_tma(ks);  // gy planes landed
+            issue(ks, tm, tm + kUC, 1024, BPL, idb, idbn, ks ? 1u : 0u);
         }
     }
 
-    // ---- forward X^T loads: item (spot k = tid / 2, column quad cq = tid % 2):
-    // gx[c0 + 8 cc + 4 cq + j][k], j < 4 ---------------------------------------
-    const int xf_k = tid >> 1, xf_cq = tid & 1;
-    const bool xf_on = xf_k < NP;
-    float2 xf[4];
-    auto load_f = [&](int cc) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int gc = min(c0 + cc * kUF + 4 * xf_cq + j, a.side - 1);
-            xf[j] = (xf_on && xf_k < n) ? __ldg(gx + (int64_t)gc * a.np + xf_k) : make_float2(0.f, 0.f);
-        }
-    };
-    load_f(0);
-
     // amplitudes of this thread's 32 pixels: columns 8 cc + 4 h + j (c0 is a
-    // multiple of 4, so each group of 4 is one aligned float4 when side % 4 == 0)
+    // multiple of 8, so each group of 4 is one aligned float4 when side % 4 == 0)
     const int64_t prow = (int64_t)min(grow, a.side - 1) * a.side;
     float br[32], bi[32];
     const bool vec_amp = (a.side & 3) == 0;
@@ -404,94 +473,90 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
     }
 
     // ---- forward: T = b X ------------------------------------------------------
-    // stage: b' planes [128 rows][8 columns] (hs_uoff), then X^T planes
-    // [NP spots][8 columns] ((k/8)*128 + (c/4)*FLBO + (k%8)*16 + (c%4)*4)
+    // A slot: b' planes [128 rows][8 columns] (hs_uoff); B slot: X^T planes
+    // [NP spots][8 columns] ((k/8)*128 + (c/4)*FLBO + (k%8)*16 + (c%4)*4), TMA
     const uint32_t idf = hs_idesc_tf32(NP, false), idfn = hs_idesc_tf32(NP, true);
 #pragma unroll
     for (int cc = 0; cc < NCC; ++cc) {
-        const int j = ksteps + cc;  // stage-sequence step
-        const int s = j % kUStages;
-        if (j >= 3) wait_mma(j - 3);  // this stage free
-        unsigned char *slot = sbase + s * kUSlot;
+        const int j = ksteps + cc;   // step
+        wait_mma(j - 2);             // A slot of j (last used by j - 4), B slot of j + 1 (j - 2) free
+        if (tid == 0) tma_ahead(j);
         {   // b' (this thread's row, columns 4h .. 4h+3 of the k-step)
             float4 rh, rl, ih, il;
             hs_split4(br[4 * cc], br[4 * cc + 1], br[4 * cc + 2], br[4 * cc + 3], rh, rl);
             hs_split4(bi[4 * cc], bi[4 * cc + 1], bi[4 * cc + 2], bi[4 * cc + 3], ih, il);
-            unsigned char *d = slot + row * 16 + h * 2048;
+            unsigned char *d = sbase + (j % kUA) * kUASlot + row * 16 + h * 2048;
             *reinterpret_cast<float4 *>(d) = rh;
             *reinterpret_cast<float4 *>(d + kUAPl) = rl;
             *reinterpret_cast<float4 *>(d + 2 * kUAPl) = ih;
             *reinterpret_cast<float4 *>(d + 3 * kUAPl) = il;
         }
-        if (xf_on) {
-            float4 rh, rl, ih, il;
-            hs_split4(xf[0].x, xf[1].x, xf[2].x, xf[3].x, rh, rl);
-            hs_split4(xf[0].y, xf[1].y, xf[2].y, xf[3].y, ih, il);
-            unsigned char *d = slot + kUBOff + (xf_k >> 3) * 128 + xf_cq * FLBO + (xf_k & 7) * 16;
-            *reinterpret_cast<float4 *>(d) = rh;
-            *reinterpret_cast<float4 *>(d + FPL) = rl;
-            *reinterpret_cast<float4 *>(d + 2 * FPL) = ih;
-            *reinterpret_cast<float4 *>(d + 3 * FPL) = il;
-        }
-        if (cc + 1 < NCC) load_f(cc + 1);
-        publish();  // (cc = 0: also orders the S reads before T overwrites S)
+        publish(j);  // (cc = 0: also orders the S reads before T overwrites S)
         if (tid == 0) {
-            const uint32_t xs = sb + s * kUSlot;
-            const uint64_t xb[4] = {hs_sdesc(xs + kUBOff, FLBO, 128), hs_sdesc(xs + kUBOff + FPL, FLBO, 128),
-                                    hs_sdesc(xs + kUBOff + 2 * FPL, FLBO, 128),
-                                    hs_sdesc(xs + kUBOff + 3 * FPL, FLBO, 128)};
-            hs_cmma(mma_ss, tm, tm + NP, [&](int pl) { return hs_sdesc(xs + pl * kUAPl, 2048, 128); }, xb, idf,
-                    idfn, cc ? 1u : 0u);
-            commit(j);
+            wait_tma(j);  // X^T planes landed
+            issue(j, tm, tm + NP, FLBO, FPL, idf, idfn, cc ? 1u : 0u);
         }
     }
     wait_mma(nsteps - 1);
 
-    // ---- E_k = sum_r gy[r][k] T[r][k]: spots KH h .. KH (h+1) of the row in
-    // two 8-aligned parts (KA + KB = KH, KA <= 32); each part is
-    // transpose-reduced over the warp's 32 rows (64 padded values -> 2 per
-    // lane), then the 4 lane-quarter warps are summed in order through shared
-    // memory.  gy comes from the planes (hi + lo), coalesced over the rows.
+    // ---- E_k = sum_r gy[r][k] T[r][k]: spots KH h .. KH (h+1) of the row, 16
+    // at a time; each group of 16 (32 values) is transpose-reduced over the
+    // warp's 32 rows (one value per lane), then the 4 lane-quarter warps are
+    // summed in order through shared memory.  gy comes from the planes
+    // (hi + lo == gy), coalesced over the rows; the next group's planes are
+    // loaded while the current one is reduced.
     float2 *out = a.f.partials + (int64_t)pat * a.f.part_stride + (int64_t)tile * a.np;
-    constexpr int KA = 8 * ((KH / 8 + 1) / 2), KB = KH - KA;
+    constexpr int NG = (KH + 15) / 16;  // groups of 16 spots (the last may hold 8)
+    float4 gq[2][2][4];                 // [buffer][quad-pair half][plane]
+    auto load_g = [&](int g, float4 (&d)[2][4]) {
+        const int kk = KH * h + 16 * g;
 #pragma unroll
-    for (int part = 0; part < 2; ++part) {
-        const int KQ = part ? KB : KA;
-        if (KQ == 0) break;  // compile-time per NP
-        const int kbase = KH * h + (part ? KA : 0);
-        float v[64];
+        for (int e = 0; e < 2; ++e) {  // k8 block e of the group
+            if (16 * g + 8 * e < KH) {
+                const float4 *pb = reinterpret_cast<const float4 *>(gyp + (int64_t)((kk + 8 * e) / kUF) * (kUASlot / 4)) + row;
 #pragma unroll
-        for (int j = 0; j < 64; ++j) v[j] = 0.f;
-#pragma unroll
-        for (int k8 = 0; k8 < 4; ++k8) {
-            if (8 * k8 < KQ) {
-                const int kk = kbase + 8 * k8;  // multiple of 8: one plane block
-                const float4 *pb = reinterpret_cast<const float4 *>(gyp + (int64_t)(kk / kUF) * (kUPlaneBlock / 4)) + row;
-                float gr[8], gi[8];
-#pragma unroll
-                for (int hq = 0; hq < 2; ++hq) {  // spots 4 hq .. 4 hq + 3 at float4 offset hq * 128
+                for (int hq = 0; hq < 2; ++hq) {
+                    // quad hq of block e -> d[e][2 hq] (re: hi + lo), d[e][2 hq + 1] (im)
                     const float4 rh = __ldg(pb + hq * 128), rl = __ldg(pb + 256 + hq * 128);
                     const float4 ih = __ldg(pb + 512 + hq * 128), il = __ldg(pb + 768 + hq * 128);
-                    gr[4 * hq] = rh.x + rl.x; gr[4 * hq + 1] = rh.y + rl.y;
-                    gr[4 * hq + 2] = rh.z + rl.z; gr[4 * hq + 3] = rh.w + rl.w;
-                    gi[4 * hq] = ih.x + il.x; gi[4 * hq + 1] = ih.y + il.y;
-                    gi[4 * hq + 2] = ih.z + il.z; gi[4 * hq + 3] = ih.w + il.w;
+                    d[e][2 * hq] = make_float4(rh.x + rl.x, rh.y + rl.y, rh.z + rl.z, rh.w + rl.w);
+                    d[e][2 * hq + 1] = make_float4(ih.x + il.x, ih.y + il.y, ih.z + il.z, ih.w + il.w);
                 }
+            }
+        }
+    };
+    load_g(0, gq[0]);
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        float4 (&gc)[2][4] = gq[g & 1];
+        if (g + 1 < NG) load_g(g + 1, gq[(g + 1) & 1]);
+        const int kk = KH * h + 16 * g;
+        const int KQ = min(16, KH - 16 * g);  // 16 or 8 (compile-time per NP)
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            if (8 * e < KQ) {
                 float tr[8], ti[8];
-                hs_tc_ld8(tl + kk, tr);
-                hs_tc_ld8(tl + NP + kk, ti);
+                hs_tc_ld8(tl + kk + 8 * e, tr);
+                hs_tc_ld8(tl + NP + kk + 8 * e, ti);
                 hs_tc_wait_ld();
+                const float gr[8] = {gc[e][0].x, gc[e][0].y, gc[e][0].z, gc[e][0].w,
+                                     gc[e][2].x, gc[e][2].y, gc[e][2].z, gc[e][2].w};
+                const float gi[8] = {gc[e][1].x, gc[e][1].y, gc[e][1].z, gc[e][1].w,
+                                     gc[e][3].x, gc[e][3].y, gc[e][3].z, gc[e][3].w};
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    v[16 * k8 + 2 * j] = fmaf(gr[j], tr[j], -gi[j] * ti[j]);
-                    v[16 * k8 + 2 * j + 1] = fmaf(gr[j], ti[j], gi[j] * tr[j]);
+                    v[16 * e + 2 * j] = fmaf(gr[j], tr[j], -gi[j] * ti[j]);
+                    v[16 * e + 2 * j + 1] = fmaf(gr[j], ti[j], gi[j] * tr[j]);
                 }
             }
         }
         // transpose-reduce: at offset o the lane keeps the half selected by
         // its lane bit o (a fixed order per value: deterministic)
 #pragma unroll
-        for (int o = 16, w = 32; o > 0; o >>= 1, w >>= 1) {
+        for (int o = 16, w = 16; o > 0; o >>= 1, w >>= 1) {
             const bool up = (lane & o) != 0;
 #pragma unroll
             for (int j = 0; j < w; ++j) {
@@ -500,22 +565,19 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
                 v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
             }
         }
-        const int base = ((lane & 16) ? 32 : 0) + ((lane & 8) ? 16 : 0) + ((lane & 4) ? 8 : 0) +
-                         ((lane & 2) ? 4 : 0) + ((lane & 1) ? 2 : 0);
-        red[warp * 64 + base] = v[0];
-        red[warp * 64 + base + 1] = v[1];
+        // lane l holds value index l (value 2 s + t = spot s, re/im t)
+        red[warp * 32 + lane] = v[0];
         __syncthreads();
-        // value 2 j (+1) of part (hq, part) is spot KH hq + kbase-offset + j
-        if (tid < 2 * 32) {
-            const int hq = tid >> 5, j = tid & 31;
-            if (j < KQ) {
+        if (tid < 2 * 16) {  // (spot-half hq, spot s of the group)
+            const int hq = tid >> 4, s = tid & 15;
+            if (s < KQ) {
                 float x = 0.f, y = 0.f;
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
-                    x += red[(qq + 4 * hq) * 64 + 2 * j];
-                    y += red[(qq + 4 * hq) * 64 + 2 * j + 1];
+                    x += red[(qq + 4 * hq) * 32 + 2 * s];
+                    y += red[(qq + 4 * hq) * 32 + 2 * s + 1];
                 }
-                out[KH * hq + (part ? KA : 0) + j] = make_float2(x, y);
+                out[KH * hq + 16 * g + s] = make_float2(x, y);
             }
         }
         __syncthreads();

@@ -1,8 +1,9 @@
-"""The tcgen05 full-range pass (csrc/hs_umma.cuh, HS_UMMA=1) under the same
-parity bar as the default FFMA tile pass: the solver cases of
+"""Both full-range pass implementations stay under the parity bar.  The
+default for np <= 112 is the tcgen05 pass (csrc/hs_umma.cuh), which the rest
+of the GPU suite exercises; this re-runs the solver cases of
 test_gpu_parity.py (golden runs, the grid100 quality gate, bitwise
-repeatability / batch invariance, c=1 == WGS) re-run in a child process with
-the tensor-core pass selected at plan creation.
+repeatability / batch invariance, c=1 == WGS) in a child process with the
+FFMA tile pass (csrc/hs_tile.cuh, HS_UMMA=0) selected at plan creation.
 """
 
 import os
@@ -17,8 +18,8 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def test_parity_with_tcgen05_full_pass():
-    env = dict(os.environ, HS_UMMA="1")
+def test_parity_with_ffma_full_pass():
+    env = dict(os.environ, HS_UMMA="0")
     r = subprocess.run(
         [sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
          os.path.join(HERE, "test_gpu_parity.py"),
