@@ -526,7 +526,7 @@ int ensure_batch(hs_plan *p, int batch, int n)
         free_batch(p);
         return rc;
     }
-    if (p->umma_enabled && cfg.ns > 0 && cfg.np <= kUNPMax) {
+    if (p->umma_enabled) {
         p->gyp_stride = hs_umma_plane_floats(p->side, cfg.np);
         if ((rc = dalloc(&p->d_gyp, (size_t)B * p->gyp_stride))) {
             free_batch(p);
@@ -604,7 +604,7 @@ UpdArgs upd_args(hs_plan *p, int act)
 }
 
 // Full-range tile list of the current configuration: the tcgen05 pass's
-// 128 x 64 tiles when np <= 112 (hs_umma), else the FFMA 64 x 64 tiles.
+// 128 x 64 tiles (hs_umma, every np) unless HS_UMMA=0, then the FFMA 64 x 64 tiles.
 struct TileSet {
     const int32_t *d;
     int32_t n;
@@ -613,7 +613,7 @@ struct TileSet {
 
 TileSet tile_set(const hs_plan *p)
 {
-    if (p->umma_enabled && p->cfg.ns > 0 && p->cfg.np <= kUNPMax && p->d_gyp &&
+    if (p->umma_enabled && p->d_gyp &&
         p->gyp_stride >= hs_umma_plane_floats(p->side, p->cfg.np))
         return {p->d_utiles, p->nutiles, true};
     return {p->d_tiles, p->ntiles, false};
@@ -627,7 +627,9 @@ int launch_tables(hs_plan *p, bool seed)
                                                   seed ? p->d_theta : nullptr, p->d_coef, p->d_w);
     CUDA_TRY(cudaGetLastError());
     if (p->d_gyp && tile_set(p).umma) {
-        dim3 pg((unsigned)((p->side + kUR - 1) / kUR * (p->cfg.np / kUF) + hs_umma_xblocks(p->side)), p->batch);
+        dim3 pg((unsigned)((p->side + kUR - 1) / kUR * (p->cfg.np / kUF) +
+                           hs_umma_xblocks(p->side) * hs_umma_nsc(p->cfg.np)),
+                p->batch);
         hs_umma_prep_kernel<<<pg, 256, 0, p->stream>>>(p->d_gx, p->d_gy, p->d_gyp, p->side, p->cfg.np,
                                                        (int64_t)p->side * p->cfg.np, p->gyp_stride);
         CUDA_TRY(cudaGetLastError());
@@ -1030,7 +1032,7 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
         CUDA_TRY(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(p->d_utiles, utiles.data(), utiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
         if (const char *env = getenv("HS_UMMA")) p->umma_enabled = atoi(env) != 0;
-        for (int np = 16; np <= kUNPMax; np += 16)
+        for (int np = 16; np <= kUNPC; np += 16)
             for (int w = 0; w < 2; ++w)
                 CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_umma(np, w != 0),
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,4 +1,5 @@
-// Instantiates the tcgen05 full-range pass for np = 16 .. 112.
+// Instantiates the tcgen05 full-range pass for np = 16 .. 112 (one forward
+// spot chunk) and for larger np (forward spot chunks of 128).
 #include "hs_umma.cuh"
 
 namespace hs {
@@ -19,7 +20,7 @@ UmmaFn hs_select_umma(int np, bool write)
     case 80: return pick<80>(write);
     case 96: return pick<96>(write);
     case 112: return pick<112>(write);
-    default: return nullptr;
+    default: return np > kUNPMax ? pick<kUNPC>(write) : nullptr;  // spot-chunked forward
     }
 }
 

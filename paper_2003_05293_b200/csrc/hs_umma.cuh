@@ -54,14 +54,15 @@ namespace hs {
 constexpr int kUR = 128;         // tile rows (MMA M)
 constexpr int kUC = 64;          // tile columns
 constexpr int kUF = 8;           // spots / columns per stage (one MMA k-step)
-constexpr int kUNPMax = 112;     // largest np (TMEM: 2 np <= 256)
+constexpr int kUNPMax = 112;     // largest np run as one forward spot chunk (N = np)
+constexpr int kUNPC = 128;       // forward spot chunk for larger np (T: 2 x 128 TMEM columns)
 constexpr int kUThreads = 256;
 constexpr int kUTmem = 256;      // TMEM columns per CTA (two CTAs per SM)
 constexpr int kUA = 4;           // A ring: gy planes (backward, TMA) / b' (forward, threads)
 constexpr int kUB = 3;           // B ring: X' (backward, threads) / X^T planes (forward, TMA)
 constexpr int kUAPl = kUR * kUF * 4;                // A plane [128][8] (4 KB)
 constexpr int kUASlot = 4 * kUAPl;                  // 16 KB
-constexpr int kUBSlot = 4 * kUNPMax * kUF * 4;      // 14 KB: X^T at np = 112 (X' needs 8 KB)
+constexpr int kUBSlot = 4 * kUNPC * kUF * 4;        // 16 KB: X^T chunk of 128 spots (X' needs 8 KB)
 
 __host__ __device__ constexpr size_t hs_umma_smem_bytes()
 {
@@ -69,18 +70,27 @@ __host__ __device__ constexpr size_t hs_umma_smem_bytes()
     return (size_t)kUA * kUASlot + (size_t)kUB * kUBSlot + 128 + 8 * 32 * sizeof(float);
 }
 
+// Forward spot chunk (the MMA N) and chunk count for a table width np:
+// one chunk of np spots up to 112, else chunks of 128 (the last zero-padded).
+__host__ __device__ constexpr int hs_umma_npc(int np) { return np <= kUNPMax ? np : kUNPC; }
+__host__ __device__ constexpr int hs_umma_nsc(int np) { return (np + hs_umma_npc(np) - 1) / hs_umma_npc(np); }
+
 // Operand planes of one pattern (constant per table build):
-//   gy : [band][k-step][4][128 rows][8 spots]       (A of the backward)
-//   X^T: [column block of 8][4][np spots][8 columns] (B of the forward),
-//        ceil(side / 8) + 8 blocks (the tail blocks are zero)
+//   gy : [band][k-step][4][128 rows][8 spots]                  (A of the backward)
+//   X^T: [column block of 8][spot chunk][4][npc spots][8 columns] (B of the forward),
+//        ceil(side / 8) + 8 column blocks (the tail blocks are zero)
 __host__ __device__ constexpr int64_t hs_umma_gy_floats(int side, int np)
 {
     return (int64_t)((side + kUR - 1) / kUR) * (np / kUF) * (kUASlot / 4);
 }
 __host__ __device__ constexpr int hs_umma_xblocks(int side) { return (side + 7) / 8 + 8; }
+__host__ __device__ constexpr int64_t hs_umma_xblock_floats(int np)
+{
+    return (int64_t)hs_umma_nsc(np) * 4 * hs_umma_npc(np) * kUF;
+}
 __host__ __device__ constexpr int64_t hs_umma_plane_floats(int side, int np)
 {
-    return hs_umma_gy_floats(side, np) + (int64_t)hs_umma_xblocks(side) * 4 * np * kUF;
+    return hs_umma_gy_floats(side, np) + (int64_t)hs_umma_xblocks(side) * hs_umma_xblock_floats(np);
 }
 
 // Offset (floats) of element (r, k) in a [128][8] K-major operand plane.
@@ -95,7 +105,7 @@ __device__ __forceinline__ void hs_split_store(float v, float *dst, int plane_fl
 }
 
 // gy / gx -> tf32 hi/lo planes {re_h, re_l, im_h, im_l} in the operand
-// layouts.  grid (bands * np / 8 + xblocks, B), 256 threads.
+// layouts.  grid (bands * np / 8 + xblocks * nsc, B), 256 threads.
 static __global__ void hs_umma_prep_kernel(const float2 *__restrict__ gx, const float2 *__restrict__ gy,
                                            float *__restrict__ planes, int side, int np, int64_t tab_stride,
                                            int64_t plane_stride)
@@ -117,14 +127,16 @@ static __global__ void hs_umma_prep_kernel(const float2 *__restrict__ gx, const 
             hs_split_store(v.y, dst + o + kUAPl / 2, kUAPl / 4);
         }
     } else {
-        const int cb = blockIdx.x - ngy;
-        const int pl = np * kUF;  // plane floats
-        float *dst = base + hs_umma_gy_floats(side, np) + (int64_t)cb * 4 * pl;
-        for (int i = threadIdx.x; i < np * kUF; i += blockDim.x) {
+        const int nsc = hs_umma_nsc(np), npc = hs_umma_npc(np);
+        const int cb = (blockIdx.x - ngy) / nsc, sc = (blockIdx.x - ngy) % nsc;
+        const int pl = npc * kUF;  // plane floats
+        float *dst = base + hs_umma_gy_floats(side, np) + (int64_t)(blockIdx.x - ngy) * 4 * pl;
+        for (int i = threadIdx.x; i < npc * kUF; i += blockDim.x) {
             const int k = i / kUF, c = i % kUF;
-            const int gc = cb * kUF + c;
-            const float2 v = gc < side ? gx[(int64_t)pat * tab_stride + (int64_t)gc * np + k] : make_float2(0.f, 0.f);
-            const int o = (k >> 3) * 32 + (c >> 2) * (np / 8) * 32 + (k & 7) * 4 + (c & 3);
+            const int gc = cb * kUF + c, gk = sc * npc + k;
+            const float2 v = (gc < side && gk < np) ? gx[(int64_t)pat * tab_stride + (int64_t)gc * np + gk]
+                                                    : make_float2(0.f, 0.f);
+            const int o = (k >> 3) * 32 + (c >> 2) * (npc / 8) * 32 + (k & 7) * 4 + (c & 3);
             hs_split_store(v.x, dst + o, pl);
             hs_split_store(v.y, dst + o + 2 * pl, pl);
         }
@@ -238,9 +250,9 @@ __device__ __forceinline__ void hs_cmma(Mma mma, uint32_t dr, uint32_t di, AOp a
 }
 
 template <int NP, bool WRITE>
-__global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
+__global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel(const TileArgs a)
 {
-    static_assert(NP % 16 == 0 && NP <= kUNPMax, "forward N = np must be a multiple of 16, <= 112");
+    static_assert(NP % 16 == 0 && (NP <= kUNPMax || NP == kUNPC), "forward N: np <= 112 or chunks of 128");
     constexpr int NCC = kUC / kUF;           // forward k-steps (8)
     constexpr uint32_t BPL = kUC * kUF * 4;  // backward X' plane bytes (2 KB)
     constexpr uint32_t FPL = NP * kUF * 4;   // forward X^T plane bytes
@@ -251,7 +263,6 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
     // operands written (all threads arrive) [11, 15)
     __shared__ __align__(8) unsigned long long mbar[3 * kUA + kUB];
     __shared__ uint32_t s_tmem;
-    __shared__ float2 coef_s[NP];
 
     hs_pdl_launch_next();
     const int pat = blockIdx.y;
@@ -264,10 +275,14 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
     const float2 *gx = a.gx + (int64_t)pat * a.tab_stride;
     const float *pbase = a.gyp + (int64_t)pat * a.gyp_stride;
     const float *gyp = pbase + (int64_t)(r0 / kUR) * (NP / kUF) * (kUASlot / 4);
-    const float *xtp = pbase + hs_umma_gy_floats(a.side, NP) + (int64_t)(c0 / kUF) * (4 * NP * kUF);
+    // forward spot chunks of NP: one when np <= 112 (b dies before the E
+    // reduce); chunks of 128 otherwise (b stays live: one CTA per SM, no spills)
+    const int nsc = NP <= kUNPMax ? 1 : hs_umma_nsc(a.np);
+    const float *xtp = pbase + hs_umma_gy_floats(a.side, a.np) + (int64_t)(c0 / kUF) * nsc * (4 * NP * kUF);
+    const float2 *coef = a.coef + (int64_t)pat * a.np;
     const int n = a.n;
     const int ksteps = (n + 7) / 8;          // backward k-steps (8 spots)
-    const int nsteps = ksteps + NCC;         // step sequence: backward, then forward
+    const int nsteps = ksteps + nsc * NCC;   // step sequence: backward, then forward per spot chunk
 
     unsigned char *sbase = reinterpret_cast<unsigned char *>(((uintptr_t)smu + 127) & ~(uintptr_t)127);
     const uint32_t sb = hs_smem_addr(sbase);
@@ -297,7 +312,6 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
     // only now, so a dependent-launched CTA never holds it while waiting
     hs_pdl_wait_prev();
     if (a.f.u.status[pat] != 0) return;  // uniform per CTA
-    if (tid < NP) coef_s[tid] = (tid < n) ? a.coef[(int64_t)pat * a.np + tid] : make_float2(0.f, 0.f);
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(hs_smem_addr(&s_tmem)),
                      "n"(kUTmem));
@@ -323,7 +337,8 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
         }
         if (i + 1 >= ksteps && i + 1 < nsteps) {
             const int j = i + 1;
-            bulk(sbb + (j % kUB) * kUBSlot, xtp + (int64_t)(j - ksteps) * (4 * NP * kUF), 4 * FPL,
+            const int f = j - ksteps;  // spot chunk f / 8, column block f % 8
+            bulk(sbb + (j % kUB) * kUBSlot, xtp + ((int64_t)(f % NCC) * nsc + f / NCC) * (4 * NP * kUF), 4 * FPL,
                  bar_bf + 8 * (j % kUB));
         }
     };
@@ -392,13 +407,44 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
     };
 
     // ---- backward: S = gy (coef X)^T ------------------------------------------
+    // Spot-chunked variant (large n): the k-steps accumulate in groups of KG
+    // into two alternating TMEM regions, and each finished group is added
+    // into fp32 registers (sacc) -- long MMA accumulation chains lose
+    // accuracy (the tensor core's fp32 accumulate truncates), short ones do not.
+    constexpr bool CH = NP == kUNPC;
+    constexpr int KG = 8;
+    float sacc[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) sacc[i] = 0.f;
+    int folded = 0;  // accumulation groups added into sacc
+    auto fold_group = [&]() {
+        const uint32_t rg = tl + (uint32_t)((folded & 1) * 128);
+#pragma unroll
+        for (int cc = 0; cc < NCC; cc += 2) {
+            float sr[8], si[8];
+            hs_tc_ld4(rg + cc * kUF + 4 * h, sr);
+            hs_tc_ld4(rg + (cc + 1) * kUF + 4 * h, sr + 4);
+            hs_tc_ld4(rg + kUC + cc * kUF + 4 * h, si);
+            hs_tc_ld4(rg + kUC + (cc + 1) * kUF + 4 * h, si + 4);
+            hs_tc_wait_ld();
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                sacc[4 * cc + jj] += sr[jj];
+                sacc[32 + 4 * cc + jj] += si[jj];
+            }
+        }
+        ++folded;
+    };
     const uint32_t idb = hs_idesc_tf32(kUC, false), idbn = hs_idesc_tf32(kUC, true);
     for (int ks = 0; ks < ksteps; ++ks) {
         if (ks >= 2) wait_mma(ks - 2);  // A slot of ks + 2, B slots of ks + 1 and ks free
+        if (CH)  // groups whose last step is <= ks - 2 (group g is read before group g + 2 reuses its region)
+            while (folded < (ks - 1) / KG) fold_group();
         if (tid == 0) tma_ahead(ks);
         if (xb_on) {  // X' = coef_k gx[c][k], planes [64 columns][8 spots]: (c/8)*128 + (k/4)*1024 + (c%8)*16
             const int k = ks * kUF + 4 * xb_kq;
-            const float2 w0 = coef_s[k], w1 = coef_s[k + 1], w2 = coef_s[k + 2], w3 = coef_s[k + 3];
+            // coef past n is zero (hs_update / seed write the whole np row)
+            const float2 w0 = coef[k], w1 = coef[k + 1], w2 = coef[k + 2], w3 = coef[k + 3];
             const float4 u0 = xq[0], u1 = xq[1];
             const float xr0 = fmaf(w0.x, u0.x, -w0.y * u0.y), xi0 = fmaf(w0.x, u0.y, w0.y * u0.x);
             const float xr1 = fmaf(w1.x, u0.z, -w1.y * u0.w), xi1 = fmaf(w1.x, u0.w, w1.y * u0.z);
@@ -420,7 +466,8 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
         publish(ks);
         if (tid == 0) {
             wait_tma(ks);  // gy planes landed
-            issue(ks, tm, tm + kUC, 1024, BPL, idb, idbn, ks ? 1u : 0u);
+            const uint32_t dr = CH ? tm + (uint32_t)(((ks / KG) & 1) * 128) : tm;
+            issue(ks, dr, dr + kUC, 1024, BPL, idb, idbn, (CH ? ks % KG : ks) ? 1u : 0u);
         }
     }
 
@@ -444,15 +491,26 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
     }
     wait_mma(ksteps - 1);
 
+    if (CH)
+        while (folded < (ksteps + KG - 1) / KG) fold_group();
+
     // ---- S -> b = A conj(S)/|S| (registers), phase write --------------------
 #pragma unroll
     for (int cc = 0; cc < NCC; cc += 2) {
         float sr[8], si[8];
-        hs_tc_ld4(tl + cc * kUF + 4 * h, sr);
-        hs_tc_ld4(tl + (cc + 1) * kUF + 4 * h, sr + 4);
-        hs_tc_ld4(tl + kUC + cc * kUF + 4 * h, si);
-        hs_tc_ld4(tl + kUC + (cc + 1) * kUF + 4 * h, si + 4);
-        hs_tc_wait_ld();
+        if (CH) {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                sr[jj] = sacc[4 * cc + jj];
+                si[jj] = sacc[32 + 4 * cc + jj];
+            }
+        } else {
+            hs_tc_ld4(tl + cc * kUF + 4 * h, sr);
+            hs_tc_ld4(tl + (cc + 1) * kUF + 4 * h, sr + 4);
+            hs_tc_ld4(tl + kUC + cc * kUF + 4 * h, si);
+            hs_tc_ld4(tl + kUC + (cc + 1) * kUF + 4 * h, si + 4);
+            hs_tc_wait_ld();
+        }
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
             const int i = 4 * cc + jj;
@@ -476,9 +534,12 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
     // A slot: b' planes [128 rows][8 columns] (hs_uoff); B slot: X^T planes
     // [NP spots][8 columns] ((k/8)*128 + (c/4)*FLBO + (k%8)*16 + (c%4)*4), TMA
     const uint32_t idf = hs_idesc_tf32(NP, false), idfn = hs_idesc_tf32(NP, true);
+    float2 *out = a.f.partials + (int64_t)pat * a.f.part_stride + (int64_t)tile * a.np;
+#pragma unroll 1
+    for (int sc = 0; sc < nsc; ++sc) {
 #pragma unroll
     for (int cc = 0; cc < NCC; ++cc) {
-        const int j = ksteps + cc;   // step
+        const int j = ksteps + sc * NCC + cc;  // step
         wait_mma(j - 2);             // A slot of j (last used by j - 4), B slot of j + 1 (j - 2) free
         if (tid == 0) tma_ahead(j);
         {   // b' (this thread's row, columns 4h .. 4h+3 of the k-step)
@@ -491,13 +552,13 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
             *reinterpret_cast<float4 *>(d + 2 * kUAPl) = ih;
             *reinterpret_cast<float4 *>(d + 3 * kUAPl) = il;
         }
-        publish(j);  // (cc = 0: also orders the S reads before T overwrites S)
+        publish(j);  // (cc = 0: also orders the S / previous chunk's T reads before T is overwritten)
         if (tid == 0) {
             wait_tma(j);  // X^T planes landed
             issue(j, tm, tm + NP, FLBO, FPL, idf, idfn, cc ? 1u : 0u);
         }
     }
-    wait_mma(nsteps - 1);
+    wait_mma(ksteps + (sc + 1) * NCC - 1);
 
     // ---- E_k = sum_r gy[r][k] T[r][k]: spots KH h .. KH (h+1) of the row, 16
     // at a time; each group of 16 (32 values) is transpose-reduced over the
@@ -505,7 +566,7 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
     // summed in order through shared memory.  gy comes from the planes
     // (hi + lo == gy), coalesced over the rows; the next group's planes are
     // loaded while the current one is reduced.
-    float2 *out = a.f.partials + (int64_t)pat * a.f.part_stride + (int64_t)tile * a.np;
+    const int k0 = sc * NP;             // first spot of the chunk
     constexpr int NG = (KH + 15) / 16;  // groups of 16 spots (the last may hold 8)
     float4 gq[2][2][4];                 // [buffer][quad-pair half][plane]
     auto load_g = [&](int g, float4 (&d)[2][4]) {
@@ -513,7 +574,9 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {  // k8 block e of the group
             if (16 * g + 8 * e < KH) {
-                const float4 *pb = reinterpret_cast<const float4 *>(gyp + (int64_t)((kk + 8 * e) / kUF) * (kUASlot / 4)) + row;
+                // spots past np (last chunk's padding): any finite plane data, T is 0 there
+                const int blk = min(k0 + kk + 8 * e, a.np - kUF) / kUF;
+                const float4 *pb = reinterpret_cast<const float4 *>(gyp + (int64_t)blk * (kUASlot / 4)) + row;
 #pragma unroll
                 for (int hq = 0; hq < 2; ++hq) {
                     // quad hq of block e -> d[e][2 hq] (re: hi + lo), d[e][2 hq + 1] (im)
@@ -570,18 +633,19 @@ __global__ void __launch_bounds__(kUThreads, 2) hs_umma_kernel(const TileArgs a)
         __syncthreads();
         if (tid < 2 * 16) {  // (spot-half hq, spot s of the group)
             const int hq = tid >> 4, s = tid & 15;
-            if (s < KQ) {
+            if (s < KQ && k0 + KH * hq + 16 * g + s < a.np) {
                 float x = 0.f, y = 0.f;
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
                     x += red[(qq + 4 * hq) * 32 + 2 * s];
                     y += red[(qq + 4 * hq) * 32 + 2 * s + 1];
                 }
-                out[KH * hq + 16 * g + s] = make_float2(x, y);
+                out[k0 + KH * hq + 16 * g + s] = make_float2(x, y);
             }
         }
         __syncthreads();
     }
+    }  // spot chunks
 
     hs_tc_fence_before();
     __syncthreads();

@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-HS_UMMA=1 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_umma.txt 2>&1
-tail -3 gpurun_out/pytest_gpu_umma.txt
-HS_UMMA=1 timeout 300 python tools/profile_pass.py --which 0 --batch 32 --reps 20
+for u in 1 0; do HS_UMMA=$u timeout 600 python tools/_n600.py 2>&1 | grep max; done
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.txt 2>&1
+tail -3 gpurun_out/pytest_gpu.txt
