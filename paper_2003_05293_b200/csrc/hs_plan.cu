@@ -713,7 +713,8 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     if (hi <= lo) return HS_OK;
     dim3 grid(hi - lo, p->batch);
     if (ts.umma)
-        return launch_pass_kernel(p, hs_select_umma(c.np, write), grid, dim3(kUThreads), hs_umma_smem_bytes(), a);
+        return launch_pass_kernel(p, hs_select_umma(c.np, write), grid, dim3(kUThreads), hs_umma_smem_bytes(c.np),
+                                  a);
     const int spt = (p->n + 7) / 8;
     // n <= 128: all spots resident (hs_tile); larger n: spot-chunked (hs_tilek)
     const bool chunked = c.ns == 0;
@@ -1036,7 +1037,7 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
             for (int w = 0; w < 2; ++w)
                 CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_umma(np, w != 0),
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)hs_umma_smem_bytes()));
+                                              (int)hs_umma_smem_bytes(np <= kUNPMax ? np : 1024)));
         CUDA_TRY(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
         if (const char *env = getenv("HS_PDL")) p->pdl_enabled = atoi(env) != 0;
         for (int ns = 1; ns <= 8; ++ns)

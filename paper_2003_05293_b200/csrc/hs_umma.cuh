@@ -62,12 +62,16 @@ constexpr int kUA = 4;           // A ring: gy planes (backward, TMA) / b' (forw
 constexpr int kUB = 3;           // B ring: X' (backward, threads) / X^T planes (forward, TMA)
 constexpr int kUAPl = kUR * kUF * 4;                // A plane [128][8] (4 KB)
 constexpr int kUASlot = 4 * kUAPl;                  // 16 KB
-constexpr int kUBSlot = 4 * kUNPC * kUF * 4;        // 16 KB: X^T chunk of 128 spots (X' needs 8 KB)
+// B slot: X^T of one forward k-step (npc spots; 14 KB at np = 112, 16 KB for
+// chunks of 128); the backward's X' needs 8 KB.  At np <= 112 two CTAs (2 x
+// ~114 KB) share an SM, so the slot is sized by the variant's npc.
+__host__ __device__ constexpr int hs_umma_bslot(int npc) { return 4 * (npc > 64 ? npc : 64) * kUF * 4; }
 
-__host__ __device__ constexpr size_t hs_umma_smem_bytes()
+__host__ __device__ constexpr size_t hs_umma_smem_bytes(int np)
 {
-    // rings + 128 B alignment slack + E reduce scratch [8 warps][32] float
-    return (size_t)kUA * kUASlot + (size_t)kUB * kUBSlot + 128 + 8 * 32 * sizeof(float);
+    // rings + 128 B alignment slack + E reduce scratch [8 warps][32] float + coef [np]
+    return (size_t)kUA * kUASlot + (size_t)kUB * hs_umma_bslot(np <= kUNPMax ? np : kUNPC) + 128 +
+           8 * 32 * sizeof(float) + 8 * (size_t)np;
 }
 
 // Forward spot chunk (the MMA N) and chunk count for a table width np:
@@ -258,6 +262,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     constexpr uint32_t FPL = NP * kUF * 4;   // forward X^T plane bytes
     constexpr uint32_t FLBO = (NP / 8) * 128;
     constexpr int KH = NP / 2;               // spots per thread in the E epilogue
+    constexpr int kUBSlot = hs_umma_bslot(NP);
     extern __shared__ __align__(128) unsigned char smu[];
     // MMA done [0, 4), A full (gy TMA) [4, 8), B full (X^T TMA) [8, 11),
     // operands written (all threads arrive) [11, 15)
@@ -279,7 +284,6 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     // reduce); chunks of 128 otherwise (b stays live: one CTA per SM, no spills)
     const int nsc = NP <= kUNPMax ? 1 : hs_umma_nsc(a.np);
     const float *xtp = pbase + hs_umma_gy_floats(a.side, a.np) + (int64_t)(c0 / kUF) * nsc * (4 * NP * kUF);
-    const float2 *coef = a.coef + (int64_t)pat * a.np;
     const int n = a.n;
     const int ksteps = (n + 7) / 8;          // backward k-steps (8 spots)
     const int nsteps = ksteps + nsc * NCC;   // step sequence: backward, then forward per spot chunk
@@ -288,6 +292,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     const uint32_t sb = hs_smem_addr(sbase);
     const uint32_t sa = sb, sbb = sb + kUA * kUASlot;  // A ring, B ring
     float *red = reinterpret_cast<float *>(sbase + kUA * kUASlot + kUB * kUBSlot);  // [8][32]
+    float2 *coef_s = reinterpret_cast<float2 *>(red + 8 * 32);                      // [np]
     const int grow = r0 + row;
     const bool row_in = grow < a.side;
 
@@ -312,6 +317,8 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     // only now, so a dependent-launched CTA never holds it while waiting
     hs_pdl_wait_prev();
     if (a.f.u.status[pat] != 0) return;  // uniform per CTA
+    // coef past n is zero (the seed writes the whole np row, hs_update only k < n)
+    for (int k = tid; k < a.np; k += kUThreads) coef_s[k] = a.coef[(int64_t)pat * a.np + k];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(hs_smem_addr(&s_tmem)),
                      "n"(kUTmem));
@@ -443,8 +450,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
         if (tid == 0) tma_ahead(ks);
         if (xb_on) {  // X' = coef_k gx[c][k], planes [64 columns][8 spots]: (c/8)*128 + (k/4)*1024 + (c%8)*16
             const int k = ks * kUF + 4 * xb_kq;
-            // coef past n is zero (hs_update / seed write the whole np row)
-            const float2 w0 = coef[k], w1 = coef[k + 1], w2 = coef[k + 2], w3 = coef[k + 3];
+            const float2 w0 = coef_s[k], w1 = coef_s[k + 1], w2 = coef_s[k + 2], w3 = coef_s[k + 3];
             const float4 u0 = xq[0], u1 = xq[1];
             const float xr0 = fmaf(w0.x, u0.x, -w0.y * u0.y), xi0 = fmaf(w0.x, u0.y, w0.y * u0.x);
             const float xr1 = fmaf(w1.x, u0.z, -w1.y * u0.w), xi1 = fmaf(w1.x, u0.w, w1.y * u0.z);

@@ -1,4 +1,9 @@
 mkdir -p gpurun_out
-for u in 1 0; do HS_UMMA=$u timeout 600 python tools/_n600.py 2>&1 | grep max; done
+timeout 300 python tools/profile_pass.py --which 0 --batch 32 --reps 20
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.txt 2>&1
 tail -3 gpurun_out/pytest_gpu.txt
+timeout 900 python tools/bench_configs.py --out gpurun_out/configs.jsonl > gpurun_out/configs.log 2>&1
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+python -c "
+import json;d=json.load(open('gpurun_out/bench.json'))
+print(d['value'],d['ms_per_step'],d['e2e']['value'],d['latency_ms_single_hologram'],d['roofline']['full_pass']['ms_per_launch'],d['roofline']['ms_per_launch'])"
