@@ -604,7 +604,7 @@ UpdArgs upd_args(hs_plan *p, int act)
 }
 
 // Full-range tile list of the current configuration: the tcgen05 pass's
-// 128 x 64 tiles (hs_umma, every np) unless HS_UMMA=0, then the FFMA 64 x 64 tiles.
+// 128 x 64 tiles (hs_umma) for n > 32 unless HS_UMMA=0, else the FFMA 64 x 64 tiles.
 struct TileSet {
     const int32_t *d;
     int32_t n;
@@ -613,7 +613,9 @@ struct TileSet {
 
 TileSet tile_set(const hs_plan *p)
 {
-    if (p->umma_enabled && p->d_gyp &&
+    // few spots: the per-tile fixed costs of the tensor-core pass outweigh its
+    // MMA speed (config 1, N = 10: 0.181 vs 0.157 ms per solve)
+    if (p->umma_enabled && p->n > 32 && p->d_gyp &&
         p->gyp_stride >= hs_umma_plane_floats(p->side, p->cfg.np))
         return {p->d_utiles, p->nutiles, true};
     return {p->d_tiles, p->ntiles, false};
