@@ -13,9 +13,11 @@
 //
 // FP32 accuracy from TF32 units: every operand is split x = hi + lo with
 // hi = rna_tf32(x), and each real product is hi*hi + hi*lo + lo*hi (the
-// dropped lo*lo term is ~2^-22 relative).  A complex MAC is four real
-// products (Sr = Vr Xr - Vi Xi: the minus via the instruction's a_negate
-// bit), so one 8-deep k-step is 12 MMAs per accumulator pair.
+// dropped lo*lo term is ~2^-22 relative).  Backward: one N = 128 MMA
+// produces [Sr | Si] from the stacked B planes [Xr; Xi] and [-Xi; Xr], so a
+// complex 8-deep k-step is 6 MMAs (A in {gr, gi} x 3 split terms).  Forward:
+// Tr and Ti are separate N = np MMAs (the minus via the a_negate bit), 12 per
+// k-step.
 //
 // Two CTAs per SM (256 TMEM columns each), so one CTA's CUDA-core phases
 // (operand builds, b, the E reduce, the fold) overlap the other's MMAs:
@@ -26,21 +28,21 @@
 // written once per table build by hs_umma_prep_kernel as tf32 hi/lo planes
 // already in the shared-memory operand layout -- gy (A of the backward,
 // [band][k-step] blocks of 16 KB) and X^T (B of the forward, 8-column blocks
-// of 14 KB) -- and each k-step's block is one TMA bulk copy; the per-pass
-// coefficients go on the B side of the backward (X' = coef_k gx[c][k],
-// built by warps 4-7) and b' (A of the forward) is written by every thread
-// for its row.  The gy planes also give the E epilogue coalesced gy reads
-// (hi + lo == gy exactly).  Shared memory: an A ring of 4 x 16 KB and a B
-// ring of 3 x 14 KB, SWIZZLE_NONE K-major canonical layout (8 x 16-byte core
-// matrices).  Per k-step every thread arrives on an operand mbarrier after
-// writing its part (no CTA-wide barrier); thread 0 waits for it and for the
-// TMA, issues the 12 MMAs and commits them to the step's MMA-done barrier;
-// the threads wait for the MMAs two steps back before reusing a slot.
+// of <= 16 KB) -- and each k-step's block is one TMA bulk copy, issued one
+// step ahead; the per-pass coefficients go on the B side of the backward
+// (X' = coef_k gx[c][k], built by warps 4-7) and b' (A of the forward) is
+// written by every thread for its row.  The gy planes also give the E
+// epilogue coalesced gy reads (hi + lo == gy exactly).  Shared memory: A and
+// B rings of 3 x 16 KB, SWIZZLE_NONE K-major canonical layout (8 x 16-byte
+// core matrices).  Per k-step every thread arrives on an operand mbarrier
+// after writing its part (no CTA-wide barrier); thread 0 waits for it and
+// for the TMA, issues the MMAs and commits them to the step's MMA-done
+// barrier; the threads wait for the MMAs two steps back before reusing a slot.
 //
-// What bounds it (ncu, B = 16): the tensor pipe is ~45% active; each
-// 128 x 64 x 8 tf32 MMA reads 6 KB of operands from shared memory, so the
-// 12-MMA complex k-step is close to shared-memory-bandwidth bound; the
-// remainder is the per-tile CUDA-core work (b, E reduce, fold).
+// What bounds it (ncu, B = 16): the tensor pipe is ~45% active; the MMAs
+// read their operands from shared memory (8 KB per backward MMA, 7.5 KB per
+// forward MMA), so a complex k-step is close to shared-memory-bandwidth
+// bound; the remainder is the per-tile CUDA-core work (b, E reduce, fold).
 //
 // Encodings (instruction descriptor, shared-memory descriptor, TMEM
 // st / ld, a_negate) are checked by tools/umma_probe.cu.
@@ -58,14 +60,13 @@ constexpr int kUNPMax = 112;     // largest np run as one forward spot chunk (N 
 constexpr int kUNPC = 128;       // forward spot chunk for larger np (T: 2 x 128 TMEM columns)
 constexpr int kUThreads = 256;
 constexpr int kUTmem = 256;      // TMEM columns per CTA (two CTAs per SM)
-constexpr int kUA = 4;           // A ring: gy planes (backward, TMA) / b' (forward, threads)
+constexpr int kUA = 3;           // A ring: gy planes (backward, TMA) / b' (forward, threads)
 constexpr int kUB = 3;           // B ring: X' (backward, threads) / X^T planes (forward, TMA)
 constexpr int kUAPl = kUR * kUF * 4;                // A plane [128][8] (4 KB)
 constexpr int kUASlot = 4 * kUAPl;                  // 16 KB
-// B slot: X^T of one forward k-step (npc spots; 14 KB at np = 112, 16 KB for
-// chunks of 128); the backward's X' needs 8 KB.  At np <= 112 two CTAs (2 x
-// ~114 KB) share an SM, so the slot is sized by the variant's npc.
-__host__ __device__ constexpr int hs_umma_bslot(int npc) { return 4 * (npc > 64 ? npc : 64) * kUF * 4; }
+// B slot: the backward's stacked X' planes ([Xr; Xi] and [-Xi; Xr], 128 rows,
+// 16 KB) or the X^T of one forward k-step (npc spots, <= 16 KB).
+__host__ __device__ constexpr int hs_umma_bslot(int) { return 4 * 2 * kUC * kUF * 4; }
 
 __host__ __device__ constexpr size_t hs_umma_smem_bytes(int np)
 {
@@ -258,7 +259,6 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
 {
     static_assert(NP % 16 == 0 && (NP <= kUNPMax || NP == kUNPC), "forward N: np <= 112 or chunks of 128");
     constexpr int NCC = kUC / kUF;           // forward k-steps (8)
-    constexpr uint32_t BPL = kUC * kUF * 4;  // backward X' plane bytes (2 KB)
     constexpr uint32_t FPL = NP * kUF * 4;   // forward X^T plane bytes
     constexpr uint32_t FLBO = (NP / 8) * 128;
     constexpr int KH = NP / 2;               // spots per thread in the E epilogue
@@ -338,12 +338,10 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     // j % 3, one step ahead (slot last used by j - 3).  Issued at step i after
     // the wait for MMA(i - 2).
     auto tma_ahead = [&](int i) {
-        if (i + 2 < ksteps) {
-            const int j = i + 2;
+        const int j = i + 1;
+        if (j < ksteps) {
             bulk(sa + (j % kUA) * kUASlot, gyp + (int64_t)j * (kUASlot / 4), kUASlot, bar_af + 8 * (j % kUA));
-        }
-        if (i + 1 >= ksteps && i + 1 < nsteps) {
-            const int j = i + 1;
+        } else if (j < nsteps) {
             const int f = j - ksteps;  // spot chunk f / 8, column block f % 8
             bulk(sbb + (j % kUB) * kUBSlot, xtp + ((int64_t)(f % NCC) * nsc + f / NCC) * (4 * NP * kUF), 4 * FPL,
                  bar_bf + 8 * (j % kUB));
@@ -354,8 +352,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
         for (int i = 0; i < kUA; ++i)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_op + 8 * i), "n"(kUThreads));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        bulk(sa, gyp, kUASlot, bar_af);  // step 0; step 1 (gy or X^T) by tma_ahead(-1)
-        tma_ahead(-1);
+        tma_ahead(-1);  // step 0's gy planes
     }
     hs_tc_fence_before();
     __syncthreads();
@@ -412,6 +409,21 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
         hs_cmma(mma_ss, dr, di, [&](int pl) { return hs_sdesc(as + pl * kUAPl, 2048, 128); }, xb, id, idn, acc);
         commit(j);
     };
+    // backward step j (thread 0): D = [Sr | Si] (N = 128) += Ar [Xr; Xi] + Ai [-Xi; Xr]
+    // with B planes {B1_h, B1_l, B2_h, B2_l} of 128 rows: 6 MMAs, no negation
+    const uint32_t idb = hs_idesc_tf32(2 * kUC, false);
+    auto issue_bwd = [&](int j, uint32_t d, uint32_t acc) {
+        const uint32_t as = sa + (j % kUA) * kUASlot, bs = sbb + (j % kUB) * kUBSlot;
+        auto A = [&](int pl) { return hs_sdesc(as + pl * kUAPl, 2048, 128); };
+        auto B = [&](int pl) { return hs_sdesc(bs + pl * kUAPl, 2048, 128); };
+        hs_mma_ss(d, A(0), B(0), idb, acc);
+        hs_mma_ss(d, A(0), B(1), idb, 1u);
+        hs_mma_ss(d, A(1), B(0), idb, 1u);
+        hs_mma_ss(d, A(2), B(2), idb, 1u);
+        hs_mma_ss(d, A(2), B(3), idb, 1u);
+        hs_mma_ss(d, A(3), B(2), idb, 1u);
+        commit(j);
+    };
 
     // ---- backward: S = gy (coef X)^T ------------------------------------------
     // Spot-chunked variant (large n): the k-steps accumulate in groups of KG
@@ -442,7 +454,6 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
         }
         ++folded;
     };
-    const uint32_t idb = hs_idesc_tf32(kUC, false), idbn = hs_idesc_tf32(kUC, true);
     for (int ks = 0; ks < ksteps; ++ks) {
         if (ks >= 2) wait_mma(ks - 2);  // A slot of ks + 2, B slots of ks + 1 and ks free
         if (CH)  // groups whose last step is <= ks - 2 (group g is read before group g + 2 reuses its region)
@@ -459,12 +470,18 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
             float4 rh, rl, ih, il;
             hs_split4(xr0, xr1, xr2, xr3, rh, rl);
             hs_split4(xi0, xi1, xi2, xi3, ih, il);
-            unsigned char *d = sbase + kUA * kUASlot + (ks % kUB) * kUBSlot + (xb_c >> 3) * 128 + xb_kq * 1024 +
-                               (xb_c & 7) * 16;
+            // planes [128 rows][8 spots] (hs_uoff): B1 = [Xr; Xi], B2 = [-Xi; Xr]
+            unsigned char *d = sbase + kUA * kUASlot + (ks % kUB) * kUBSlot + xb_c * 16 + xb_kq * 2048;
+            constexpr int R64 = kUC * 16;  // row 64
+            const float4 nih = make_float4(-ih.x, -ih.y, -ih.z, -ih.w), nil = make_float4(-il.x, -il.y, -il.z, -il.w);
             *reinterpret_cast<float4 *>(d) = rh;
-            *reinterpret_cast<float4 *>(d + BPL) = rl;
-            *reinterpret_cast<float4 *>(d + 2 * BPL) = ih;
-            *reinterpret_cast<float4 *>(d + 3 * BPL) = il;
+            *reinterpret_cast<float4 *>(d + R64) = ih;
+            *reinterpret_cast<float4 *>(d + kUAPl) = rl;
+            *reinterpret_cast<float4 *>(d + kUAPl + R64) = il;
+            *reinterpret_cast<float4 *>(d + 2 * kUAPl) = nih;
+            *reinterpret_cast<float4 *>(d + 2 * kUAPl + R64) = rh;
+            *reinterpret_cast<float4 *>(d + 3 * kUAPl) = nil;
+            *reinterpret_cast<float4 *>(d + 3 * kUAPl + R64) = rl;
         }
         xq[0] = xn[0];
         xq[1] = xn[1];
@@ -473,7 +490,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
         if (tid == 0) {
             wait_tma(ks);  // gy planes landed
             const uint32_t dr = CH ? tm + (uint32_t)(((ks / KG) & 1) * 128) : tm;
-            issue(ks, dr, dr + kUC, 1024, BPL, idb, idbn, (CH ? ks % KG : ks) ? 1u : 0u);
+            issue_bwd(ks, dr, (CH ? ks % KG : ks) ? 1u : 0u);
         }
     }
 
@@ -517,6 +534,22 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
             hs_tc_ld4(tl + kUC + (cc + 1) * kUF + 4 * h, si + 4);
             hs_tc_wait_ld();
         }
+        int dix[8];  // storage indices of the 8 pixels (WRITE), two aligned int4 when side % 4 == 0
+        if (WRITE) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int c = c0 + (cc + u) * kUF + 4 * h;
+                if (vec_amp) {
+                    const int4 v = (row_in && c < a.side) ? __ldg(reinterpret_cast<const int4 *>(a.idx_img + prow + c))
+                                                          : make_int4(-1, -1, -1, -1);
+                    dix[4 * u] = v.x; dix[4 * u + 1] = v.y; dix[4 * u + 2] = v.z; dix[4 * u + 3] = v.w;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        dix[4 * u + j] = (row_in && c + j < a.side) ? __ldg(a.idx_img + prow + c + j) : -1;
+                }
+            }
+        }
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
             const int i = 4 * cc + jj;
@@ -525,7 +558,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
             if (WRITE) {
                 const int c = c0 + (i / 4) * kUF + 4 * h + (i % 4);
                 if (row_in && c < a.side) {
-                    const int32_t di = __ldg(a.idx_img + prow + c);
+                    const int32_t di = dix[jj];
                     if (di >= 0) {
                         const double ph = hs_phase_f64(sr[jj], si[jj]);
                         a.phase_out[(int64_t)pat * a.phase_stride + di] = ph;
