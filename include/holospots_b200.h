@@ -208,7 +208,8 @@ int hs_padded_spots(hs_plan *plan);
  * kernels the last solve launched, and the mean device time (CUDA events,
  * `reps` back-to-back launches on the plan stream) of the kernel `which`
  * (0 = full-range fused pass, 1 = compressed-window fused pass,
- * 2 = weight update) with the current spot batch. */
+ * 2 = full-range fused pass of the final iteration, with the f64 phase
+ * written in storage order) with the current spot batch. */
 void *hs_plan_stream(hs_plan *plan);
 int hs_last_launch_count(hs_plan *plan, int64_t *launches);
 int hs_time_kernel(hs_plan *plan, int which, int64_t subset, int reps,

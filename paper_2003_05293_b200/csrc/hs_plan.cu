@@ -1795,7 +1795,7 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
     int rc;
     if ((rc = check_device(p)) || (rc = ensure_tables(p))) return rc;
     const DevList *l;
-    if (which == 0) {
+    if (which == 0 || which == 2) {
         rc = get_dense(p, p->cfg.spw, &l);
     } else {
         if (subset < 1 || subset > p->m) return fail(HS_EINVAL, "subset invalid");
@@ -1808,6 +1808,7 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
     const UpdArgs u = upd_args(p, ACT_FIELDS);
     auto once = [&]() -> int {
         if (which == 0) return launch_tile(p, false, u, nullptr);
+        if (which == 2) return launch_tile(p, true, u, p->d_out[0]);  // final pass: phase write
         return launch_pass(p, PM_BWD | PM_FWD, *l, 0, l->count, 0, nullptr, nullptr, 0, u);
     };
     if ((rc = reset_status(p)) || (rc = once())) return rc;
@@ -1821,7 +1822,7 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *ms_per_launch = ms / reps;
-    const int64_t pixels = (which == 0) ? p->m : subset;
+    const int64_t pixels = (which != 1) ? p->m : subset;
     *pairs_per_launch = (double)pixels * p->n * p->batch;
     return HS_OK;
 }
