@@ -32,7 +32,7 @@
 // step ahead; the per-pass coefficients go on the B side of the backward
 // (X' = coef_k gx[c][k], built by warps 4-7) and b' (A of the forward) is
 // written by every thread for its row.  The gy planes also give the E
-// epilogue coalesced gy reads (hi + lo == gy exactly).  Shared memory: A and
+// epilogue coalesced gy reads (hi + lo == gy to 2^-22).  Shared memory: A and
 // B rings of 3 x 16 KB, SWIZZLE_NONE K-major canonical layout (8 x 16-byte
 // core matrices).  Per k-step every thread arrives on an operand mbarrier
 // after writing its part (no CTA-wide barrier); thread 0 waits for it and
@@ -103,10 +103,11 @@ __host__ __device__ constexpr int hs_uoff(int r, int k) { return r * 4 + (k >> 2
 
 __device__ __forceinline__ void hs_split_store(float v, float *dst, int plane_floats)
 {
-    uint32_t h;
+    uint32_t h, l;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(v - __uint_as_float(h)));
     dst[0] = __uint_as_float(h);
-    dst[plane_floats] = v - __uint_as_float(h);
+    dst[plane_floats] = __uint_as_float(l);
 }
 
 // gy / gx -> tf32 hi/lo planes {re_h, re_l, im_h, im_l} in the operand
@@ -215,10 +216,12 @@ __device__ __forceinline__ float hs_tf32_hi(float x)
 }
 
 // hi/lo split of 4 values into two float4
+// (lo is rounded to tf32 as well: the tensor core would otherwise truncate
+// its low mantissa bits, a bias that grows linearly in long sums)
 __device__ __forceinline__ void hs_split4(float a, float b, float c, float d, float4 &hi, float4 &lo)
 {
     hi = make_float4(hs_tf32_hi(a), hs_tf32_hi(b), hs_tf32_hi(c), hs_tf32_hi(d));
-    lo = make_float4(a - hi.x, b - hi.y, c - hi.z, d - hi.w);
+    lo = make_float4(hs_tf32_hi(a - hi.x), hs_tf32_hi(b - hi.y), hs_tf32_hi(c - hi.z), hs_tf32_hi(d - hi.w));
 }
 
 __device__ __forceinline__ void hs_mbar_wait(uint32_t bar, uint32_t parity)
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     const int r0 = packed >> 16, c0 = packed & 0xffff;  // c0: multiple of 8
     const float2 *gx = a.gx + (int64_t)pat * a.tab_stride;
     const float *pbase = a.gyp + (int64_t)pat * a.gyp_stride;
-    const float *gyp = pbase + (int64_t)(r0 / kUR) * (NP / kUF) * (kUASlot / 4);
+    const float *gyp = pbase + (int64_t)(r0 / kUR) * (a.np / kUF) * (kUASlot / 4);
     // forward spot chunks of NP: one when np <= 112 (b dies before the E
     // reduce); chunks of 128 otherwise (b stays live: one CTA per SM, no spills)
     const int nsc = NP <= kUNPMax ? 1 : hs_umma_nsc(a.np);
@@ -603,7 +606,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     // at a time; each group of 16 (32 values) is transpose-reduced over the
     // warp's 32 rows (one value per lane), then the 4 lane-quarter warps are
     // summed in order through shared memory.  gy comes from the planes
-    // (hi + lo == gy), coalesced over the rows; the next group's planes are
+    // (hi + lo == gy to 2^-22), coalesced over the rows; the next group's planes are
     // loaded while the current one is reduced.
     const int k0 = sc * NP;             // first spot of the chunk
     constexpr int NG = (KH + 15) / 16;  // groups of 16 spots (the last may hold 8)
