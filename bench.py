@@ -377,7 +377,8 @@ def run_ours(args):
                      "frac": achieved_win / peak,
                      "traffic": traffic.get("window_pass_dram_bytes_per_launch"),
                      "kernel": "hs_slab_kernel<7> compressed-window fused pass (backward + "
-                               "forward + fold/update), dominant: 19 of 22 launches per step",
+                               "forward + fold/update), dominant: 38 of 44 launches per step "
+                               "(two graph branches of 16 patterns)",
                      "peak_source": "measured FP32 FFMA microbenchmark (hs_fma_peak, "
                                     "MEASURED_PEAKS.json has no FP32 figure)",
                      "algorithmic_flop_per_launch": flops_win,

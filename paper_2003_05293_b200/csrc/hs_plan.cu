@@ -1317,10 +1317,11 @@ static int solve_into(hs_plan *p, int alg, int iters, int64_t subset, const doub
     p->last_alg = alg;
     p->last_iters = iters;
     p->last_flags = flags;
-    {   // tables(+seed) + passes, per graph branch
+    {   // tables(+seed) [+ tcgen05 operand planes] + passes, per graph branch
         static const bool no_split = getenv("HS_SPLIT") && atoi(getenv("HS_SPLIT")) == 0;
         const int branches = (p->batch >= kSplitBatch && !no_split) ? 2 : 1;
-        p->last_launches = 1 + (int64_t)branches * ((alg == HS_ALG_RS) ? 1 : iters + 1);
+        const int prep = (p->d_gyp && tile_set(p).umma) ? 1 : 0;
+        p->last_launches = 1 + prep + (int64_t)branches * ((alg == HS_ALG_RS) ? 1 : iters + 1);
     }
     return HS_OK;
 }
