@@ -1,1 +1,2 @@
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()"
+timeout 300 python tools/_d2h.py
+nvidia-smi -q | grep -iE "Link Gen|Link Width|Max|Current" | head -12
