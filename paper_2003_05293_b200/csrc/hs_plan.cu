@@ -155,6 +155,7 @@ struct hs_plan {
     int32_t *d_utiles = nullptr;          // non-empty 128x64 tiles of the tcgen05 full pass
     int32_t nutiles = 0;
     bool umma_enabled = true;             // HS_UMMA=0: FFMA tiles (hs_tile) for every n
+    int umma_max_n = 128;                 // largest n on the tensor cores (HS_UMMA_MAXN, experiments)
     int num_sms = 148;
     bool pdl = false;                     // next pass launch: programmatic dependent launch
     int view0 = 0;                        // first pattern of the sub-batch being recorded
@@ -620,7 +621,7 @@ TileSet tile_set(const hs_plan *p)
     // n = 128 that is <= 4e-6 (tolerance 1e-4), at n = 200 / 600 the weights
     // drift past 1e-4 over the iterations where the FFMA tiles stay inside
     // (tests/test_gpu_spot_chunks.py), so larger n run the FFMA tiles.
-    if (p->umma_enabled && p->n > 32 && p->n <= 128 && p->d_gyp &&
+    if (p->umma_enabled && p->n > 32 && p->n <= p->umma_max_n && p->d_gyp &&
         p->gyp_stride >= hs_umma_plane_floats(p->side, p->cfg.np))
         return {p->d_utiles, p->nutiles, true};
     return {p->d_tiles, p->ntiles, false};
@@ -1040,6 +1041,7 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
         CUDA_TRY(cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(p->d_utiles, utiles.data(), utiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
         if (const char *env = getenv("HS_UMMA")) p->umma_enabled = atoi(env) != 0;
+        if (const char *env = getenv("HS_UMMA_MAXN")) p->umma_max_n = atoi(env);
         for (int np = 16; np <= kUNPC; np += 16)
             for (int w = 0; w < 2; ++w)
                 CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_umma(np, w != 0),
