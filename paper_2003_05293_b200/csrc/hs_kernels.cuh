@@ -134,10 +134,37 @@ __device__ __forceinline__ double hs_wrap(double t)
 // widened values outside [-pi, pi) are +-pi_f32 themselves: the wrap is
 // decided in fp32 and its two results are the fp64 constants pi_f32 - 2 pi
 // and -pi_f32 + 2 pi (the same bits as wrapping the widened value).
+// atan2 for finite (y, x) != (0, 0): octant reduction r = min/max in [0, 1],
+// atan(r) = r P(r^2) with a degree-8 least-squares fit (max |error| of the
+// fp32 evaluation 2.8e-7 rad over 2M random points, the same as fp32 atan2's
+// own; fitted by tools/atan2_fit.py), then the quadrant fix-ups.  About half
+// the instructions of atan2f (no IEEE division).  Signed zeros as atan2:
+// atan2(+0, x < 0) = +pi_f32, atan2(-0, x < 0) = -pi_f32.
+__device__ __forceinline__ float hs_atan2(float y, float x)
+{
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    const float r = mn * __frcp_rn(mx);
+    const float s = r * r;
+    float p = 0.0029035801999270916f;
+    p = fmaf(p, s, -0.016283102333545685f);
+    p = fmaf(p, s, 0.04303948953747749f);
+    p = fmaf(p, s, -0.07533683627843857f);
+    p = fmaf(p, s, 0.1065467968583107f);
+    p = fmaf(p, s, -0.14207133650779724f);
+    p = fmaf(p, s, 0.19993053376674652f);
+    p = fmaf(p, s, -0.3333309292793274f);
+    p = fmaf(p, s, 1.0f);
+    float a = r * p;
+    if (ay > ax) a = 1.57079637050628662f - a;
+    if (x < 0.f) a = 3.14159274101257324f - a;
+    return copysignf(a, y);
+}
+
 __device__ __forceinline__ double hs_phase_f64(float x, float y)
 {
     if (x == 0.f && y == 0.f) return 0.0;
-    const float p = atan2f(y, x);
+    const float p = hs_atan2(y, x);
     if (p == 3.14159274101257324f) return 3.14159274101257324 - kTwoPi;
     if (p == -3.14159274101257324f) return -3.14159274101257324 + kTwoPi;
     return (double)p;
