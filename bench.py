@@ -204,8 +204,8 @@ def umma_roofline(pupil, batch, n, ms):
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense tf32 = half of bf16)"
             if bf16 else "B200_PROFILING.md nominal dense tf32 1.1 PFLOP/s",
-            "note": "k-steps are shared-memory-operand bound (6-7.5 KB of smem reads per MMA); "
-                    "ncu: tensor pipe ~45% active"}
+            "note": "ncu: tensor pipe ~39% active, tensor-core shared-memory operand reads ~32%; "
+                    "the per-tile CUDA-core work (b, E reduce, fold) fills the rest"}
 
 
 def run_ours(args):
