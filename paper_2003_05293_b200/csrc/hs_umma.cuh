@@ -1,9 +1,10 @@
 // hs_umma.cuh -- full-range fused pass on the tcgen05 tensor cores.
 //
 // Same pass as hs_tile.cuh (backward kernels.py:99-119, b = A conj(S)/|S|
-// kernels.py:136-137, forward kernels.py:122-144) for np <= 112, with both
-// complex GEMMs of a 128-row x 64-column tile issued as tcgen05.mma
-// kind::tf32 (M = 128) and accumulated in TMEM:
+// kernels.py:136-137, forward kernels.py:122-144) -- selected for 32 < n <=
+// 128 (hs_plan.cu tile_set) -- with both complex GEMMs of a 128-row x
+// 64-column tile issued as tcgen05.mma kind::tf32 (M = 128) and accumulated
+// in TMEM:
 //
 //   backward  S[r][c] = sum_k gy[r0+r][k] X'[c][k]   gy planes (A, smem, TMA)
 //                                                    X' = coef_k gx[c0+c][k] (B, smem)
@@ -23,6 +24,8 @@
 // (operand builds, b, the E reduce, the fold) overlap the other's MMAs:
 //   TMEM [0, 128)     S = {Sr, Si} x 64 columns                            backward
 //        [0, 2 NP)    T = {Tr, Ti} x NP spots                              forward
+// (np = 128 runs the spot-chunked variant NP = 128: T fills all 256 columns,
+// one CTA per SM, the backward's k-steps summed in groups in registers.)
 // S is read once into registers (b: 32 columns per thread), which frees the
 // columns T reuses.  The operands that do not change between passes are
 // written once per table build by hs_umma_prep_kernel as tf32 hi/lo planes
@@ -39,10 +42,10 @@
 // for the TMA, issues the MMAs and commits them to the step's MMA-done
 // barrier; the threads wait for the MMAs two steps back before reusing a slot.
 //
-// What bounds it (ncu, B = 16): the tensor pipe is ~45% active; the MMAs
-// read their operands from shared memory (8 KB per backward MMA, 7.5 KB per
-// forward MMA), so a complex k-step is close to shared-memory-bandwidth
-// bound; the remainder is the per-tile CUDA-core work (b, E reduce, fold).
+// What bounds it (ncu, B = 16, profiles/round1/umma_full_pass.md): the
+// tensor pipe is ~39% active and its shared-memory operand reads ~32% (8 KB
+// per backward MMA, 7.5 KB per forward MMA); the per-tile CUDA-core work (b,
+// E reduce, fold) and the mbarrier waits make up the rest.
 //
 // Encodings (instruction descriptor, shared-memory descriptor, TMEM
 // st / ld, a_negate) are checked by tools/umma_probe.cu.
