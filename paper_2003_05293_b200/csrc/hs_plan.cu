@@ -160,7 +160,9 @@ struct hs_plan {
     bool pdl = false;                     // next pass launch: programmatic dependent launch
     int view0 = 0;                        // first pattern of the sub-batch being recorded
     cudaStream_t stream2 = nullptr;       // second branch of a split solve graph
-    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    cudaStream_t stream3 = nullptr;       // tcgen05 operand-plane prep, beside the first passes
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr, prep_ev = nullptr;
+    bool prep_pending = false;            // recording: full passes must wait for prep_ev
     bool pdl_enabled = true;              // HS_PDL=0 disables
     DevList storage;                      // storage order
     std::map<int, DevList> dense;         // full range, banded layout per slots-per-warp
@@ -627,14 +629,14 @@ TileSet tile_set(const hs_plan *p)
     return {p->d_tiles, p->ntiles, false};
 }
 
-int launch_tables(hs_plan *p, bool seed)
+int launch_tables(hs_plan *p, bool seed, bool with_prep = true)
 {
     dim3 grid(p->side, p->batch);
     hs_tables_kernel<<<grid, 128, 0, p->stream>>>(p->side, p->cfg.np, p->n, p->d_axis, p->c1, p->c2, p->d_x,
                                                   p->d_y, p->d_z, p->d_gx, p->d_gy, p->d_a0,
                                                   seed ? p->d_theta : nullptr, p->d_coef, p->d_w);
     CUDA_TRY(cudaGetLastError());
-    if (p->d_gyp && tile_set(p).umma) {
+    if (with_prep && p->d_gyp && tile_set(p).umma) {
         dim3 pg((unsigned)((p->side + kUR - 1) / kUR * (p->cfg.np / kUF) +
                            hs_umma_xblocks(p->side) * hs_umma_nsc(p->cfg.np)),
                 p->batch);
@@ -720,9 +722,11 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     a.n = p->n;
     if (hi <= lo) return HS_OK;
     dim3 grid(hi - lo, p->batch);
-    if (ts.umma)
+    if (ts.umma) {
+        if (p->prep_pending) CUDA_TRY(cudaStreamWaitEvent(p->stream, p->prep_ev, 0));  // operand planes ready
         return launch_pass_kernel(p, hs_select_umma(c.np, write), grid, dim3(kUThreads), hs_umma_smem_bytes(c.np),
                                   a);
+    }
     const int spt = (p->n + 7) / 8;
     // n <= 128: all spots resident (hs_tile); larger n: spot-chunked (hs_tilek)
     const bool chunked = c.ns == 0;
@@ -894,11 +898,40 @@ int record_passes(hs_plan *p, int alg, int iters, int64_t subset, int flags, dou
 // batch on two streams): every pass ends in a partly filled wave and a
 // serial fold tail, which the other branch's passes fill (+6% at B = 32).
 // Patterns never interact, so the split cannot change any result.
+int record_solve_passes(hs_plan *p, int alg, int iters, int64_t subset, int flags, double *out);
+
 int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags, double *out)
 {
     int rc;
     if ((rc = reset_status(p))) return rc;
-    if ((rc = launch_tables(p, true))) return rc;
+    if ((rc = launch_tables(p, true, false))) return rc;
+    // the tcgen05 operand planes are first read by the full passes at the end
+    // of the schedule: prepare them on a side stream beside the window passes
+    if (p->d_gyp && tile_set(p).umma) {
+        CUDA_TRY(cudaEventRecord(p->fork_ev, p->stream));
+        CUDA_TRY(cudaStreamWaitEvent(p->stream3, p->fork_ev, 0));
+        dim3 pg((unsigned)((p->side + kUR - 1) / kUR * (p->cfg.np / kUF) +
+                           hs_umma_xblocks(p->side) * hs_umma_nsc(p->cfg.np)),
+                p->batch);
+        hs_umma_prep_kernel<<<pg, 256, 0, p->stream3>>>(p->d_gx, p->d_gy, p->d_gyp, p->side, p->cfg.np,
+                                                        (int64_t)p->side * p->cfg.np, p->gyp_stride);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaEventRecord(p->prep_ev, p->stream3));
+        p->prep_pending = true;
+    }
+    const bool prep = p->prep_pending;
+    rc = record_solve_passes(p, alg, iters, subset, flags, out);
+    p->prep_pending = false;
+    if (rc) return rc;
+    // rejoin the side stream even when no tcgen05 pass waited on it (e.g. an
+    // RS solve without fields runs its final pass on the row-run kernel)
+    if (prep) CUDA_TRY(cudaStreamWaitEvent(p->stream, p->prep_ev, 0));
+    return HS_OK;
+}
+
+int record_solve_passes(hs_plan *p, int alg, int iters, int64_t subset, int flags, double *out)
+{
+    int rc;
     if (flags & HS_WANT_RASTER)
         CUDA_TRY(cudaMemsetAsync(p->d_raster, 0, (size_t)p->batch * p->side * p->side, p->stream));
     static const bool no_split = getenv("HS_SPLIT") && atoi(getenv("HS_SPLIT")) == 0;
@@ -973,6 +1006,8 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
     CUDA_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->stream3, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&p->prep_ev, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&p->fork_ev, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&p->join_ev, cudaEventDisableTiming));
     for (int k = 0; k < 2; ++k) {
@@ -1097,6 +1132,8 @@ void hs_plan_destroy(hs_plan *p)
     cudaStreamDestroy(p->stream);
     cudaStreamDestroy(p->copy_stream);
     cudaStreamDestroy(p->stream2);
+    cudaStreamDestroy(p->stream3);
+    cudaEventDestroy(p->prep_ev);
     cudaEventDestroy(p->fork_ev);
     cudaEventDestroy(p->join_ev);
     for (int k = 0; k < 2; ++k) {

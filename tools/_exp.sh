@@ -1,2 +1,6 @@
-# scratch driver for one gpurun experiment (the last one run is kept here)
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 10 --warmup 3 > gpurun_out/b2.json 2> gpurun_out/b2.err
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.txt 2>&1
+tail -3 gpurun_out/pytest_gpu.txt
+for r in 1 2; do timeout 600 python bench.py --no-cpu > gpurun_out/bench.json 2> gpurun_out/bench.err
+python -c "
+import json;d=json.load(open('gpurun_out/bench.json'))
+print(d['value'],d['ms_per_step'],d['e2e']['value'],d['latency_ms_single_hologram'],d['gpu_launches'])"; done
