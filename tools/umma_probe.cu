@@ -10,6 +10,11 @@
 //                                               not be: 4 MN x 8 K core matrices)
 // T3  D[128x64]  = A_tmem[128xK] B[64xK]^T     A from TMEM (tcgen05.st)
 // T4  D         -= A B^T                       a_negate bit
+//
+// Last run on a B200 (round 1): T1, T3, T4 ok; T2 FAILS -- the MN-major
+// operand encoding tried here is wrong, so the kernels use K-major operands
+// only (hs_umma.cuh).  a_negate with A in shared memory (the forward pass)
+// is covered by the GPU parity tests rather than by this probe.
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
