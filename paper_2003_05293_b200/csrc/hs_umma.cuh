@@ -73,9 +73,9 @@ __host__ __device__ constexpr int hs_umma_bslot(int) { return 4 * 2 * kUC * kUF 
 
 __host__ __device__ constexpr size_t hs_umma_smem_bytes(int np)
 {
-    // rings + 128 B alignment slack + E reduce scratch [8 warps][32] float + coef [np]
+    // rings + 128 B alignment slack + E reduce scratch [2][8 warps][32] float + coef [np]
     return (size_t)kUA * kUASlot + (size_t)kUB * hs_umma_bslot(np <= kUNPMax ? np : kUNPC) + 128 +
-           8 * 32 * sizeof(float) + 8 * (size_t)np;
+           2 * 8 * 32 * sizeof(float) + 8 * (size_t)np;
 }
 
 // Forward spot chunk (the MMA N) and chunk count for a table width np:
@@ -297,8 +297,9 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     unsigned char *sbase = reinterpret_cast<unsigned char *>(((uintptr_t)smu + 127) & ~(uintptr_t)127);
     const uint32_t sb = hs_smem_addr(sbase);
     const uint32_t sa = sb, sbb = sb + kUA * kUASlot;  // A ring, B ring
-    float *red = reinterpret_cast<float *>(sbase + kUA * kUASlot + kUB * kUBSlot);  // [8][32]
-    float2 *coef_s = reinterpret_cast<float2 *>(red + 8 * 32);                      // [np]
+    float *red = reinterpret_cast<float *>(sbase + kUA * kUASlot + kUB * kUBSlot);  // [2][8][32]
+    float2 *coef_s = reinterpret_cast<float2 *>(red + 2 * 8 * 32);                  // [np]
+    int redbuf = 0;  // E reduce scratch buffer, alternating per group of 16 spots
     const int grow = r0 + row;
     const bool row_in = grow < a.side;
 
@@ -673,8 +674,12 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
                 v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
             }
         }
-        // lane l holds value index l (value 2 s + t = spot s, re/im t)
-        red[warp * 32 + lane] = v[0];
+        // lane l holds value index l (value 2 s + t = spot s, re/im t).  Two
+        // alternating buffers: one barrier per group (a buffer is rewritten
+        // two groups later, after the next group's barrier)
+        float *rb = red + redbuf * 256;
+        redbuf ^= 1;
+        rb[warp * 32 + lane] = v[0];
         __syncthreads();
         if (tid < 2 * 16) {  // (spot-half hq, spot s of the group)
             const int hq = tid >> 4, s = tid & 15;
@@ -682,13 +687,12 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
                 float x = 0.f, y = 0.f;
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
-                    x += red[(qq + 4 * hq) * 32 + 2 * s];
-                    y += red[(qq + 4 * hq) * 32 + 2 * s + 1];
+                    x += rb[(qq + 4 * hq) * 32 + 2 * s];
+                    y += rb[(qq + 4 * hq) * 32 + 2 * s + 1];
                 }
                 out[k0 + KH * hq + 16 * g + s] = make_float2(x, y);
             }
         }
-        __syncthreads();
     }
     }  // spot chunks
 

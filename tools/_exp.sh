@@ -1,4 +1,2 @@
 # scratch driver for one gpurun experiment (the last one run is kept here)
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.txt 2>&1
-tail -3 gpurun_out/pytest_gpu.txt
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()"
+for w in 0 2; do timeout 300 python tools/profile_pass.py --which $w --batch 32 --reps 20; done
