@@ -143,7 +143,11 @@ __device__ __forceinline__ double hs_wrap(double t)
 __device__ __forceinline__ float hs_atan2(float y, float x)
 {
     const float ax = fabsf(x), ay = fabsf(y);
-    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    if (mx < 1.0e-30f) {  // keep 1 / mx finite for tiny (denormal) arguments
+        mx *= 18446744073709551616.0f;
+        mn *= 18446744073709551616.0f;
+    }
     const float r = mn * __frcp_rn(mx);
     const float s = r * r;
     float p = 0.0029035801999270916f;
