@@ -59,6 +59,15 @@ extern "C" {
 #define HS_WANT_FIELDS 1   /* fuse the full-range e/u projection into the last pass */
 #define HS_WANT_RASTER 2   /* also write the SLM gray raster (default linear LUT) */
 
+/* Pixel-pass arithmetic (hs_set_precision).  The reference computes in fp64
+ * throughout (holospots/kernels.py:78-144).  FP32: fp32 pixel products with
+ * fp64 tables / folds / updates (the fast kernels).  FP64: every pixel
+ * product in fp64.  AUTO (default): FP64 when the smallest pixel set a call
+ * projects over has fewer than 512 pixels per spot, or n > 1024; else FP32. */
+#define HS_PREC_AUTO 0
+#define HS_PREC_FP32 1
+#define HS_PREC_FP64 2
+
 typedef struct hs_plan hs_plan;
 
 /* Human-readable message for the last failing call on this thread. */
@@ -67,7 +76,8 @@ const char *hs_last_error(void);
 /* Number of visible CUDA devices (0 on a host without a GPU). */
 int hs_device_count(int *count);
 
-/* Largest spot count one pattern may carry. */
+/* Largest spot count one pattern may carry (4096; above 1024 spots the
+ * passes run in fp64). */
 int hs_max_spots(void);
 
 /* Upload pupil geometry once.  rows/cols/amplitude: m storage-order pixels;
@@ -79,6 +89,13 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows,
                    const double *axis, double prism, double lens,
                    double sum_amplitude, hs_plan **out);
 void hs_plan_destroy(hs_plan *plan);
+
+/* Precision mode of the plan's pixel passes (HS_PREC_*); the environment
+ * variable HS_PRECISION=auto|fp32|fp64 sets the default of new plans.
+ * hs_get_precision: the mode, and the precision the last solve ran in
+ * (HS_PREC_FP32 or HS_PREC_FP64). */
+int hs_set_precision(hs_plan *plan, int mode);
+int hs_get_precision(hs_plan *plan, int *mode, int *last_solve);
 
 /* Spot targets of `batch` independent patterns with n spots each:
  * x, y, z, a0 are [batch][n].  Builds the per-pattern phasor tables on

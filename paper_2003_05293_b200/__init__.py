@@ -27,7 +27,8 @@ from .simulate import FieldImage, probe_intensities, render_plane
 from .sweeps import (BenchRecord, BudgetComparison, CellStats, calibrate_ops_per_ms,
                      compare_at_budget, frame_budget_ops, summarize, sweep)
 from .slm import PhaseLut, slm_raster, solve_rasters
-from ._lib import get_device, set_device
+from ._lib import get_device, get_precision, set_device, set_precision
+from .precision import precision
 from .workloads import grid_spots, named_spots, random_foci
 
 __version__ = "0.1.0"

@@ -25,6 +25,8 @@ HS_OK, HS_EINVAL, HS_EGEOMETRY, HS_EDEGENERATE, HS_EDIVERGED, HS_ECUDA, \
 ALG_RS, ALG_WGS, ALG_CSWGS = 0, 1, 2
 WANT_FIELDS = 1
 WANT_RASTER = 2
+PREC_AUTO, PREC_FP32, PREC_FP64 = 0, 1, 2
+PRECISIONS = {"auto": PREC_AUTO, "fp32": PREC_FP32, "fp64": PREC_FP64}
 
 _ERRORS = {
     HS_EINVAL: InvalidParameterError,
@@ -46,6 +48,7 @@ EXPORTS = (
     "hs_host_free", "hs_probe", "hs_solve_host_async", "hs_shard_begin", "hs_shard_pass",
     "hs_shard_update", "hs_padded_spots", "hs_shard_groups", "hs_raster", "hs_get_raster",
     "hs_shard_p2p_setup", "hs_shard_p2p_open", "hs_shard_p2p_pass", "hs_shard_p2p_close",
+    "hs_set_precision", "hs_get_precision",
 )
 
 IPC_HANDLE_BYTES = 64  # HS_IPC_HANDLE_BYTES
@@ -104,6 +107,8 @@ def load():
             "hs_shard_p2p_open": (I, [P, P]),
             "hs_shard_p2p_pass": (I, [P, I]),
             "hs_shard_p2p_close": (I, [P]),
+            "hs_set_precision": (I, [P, I]),
+            "hs_get_precision": (I, [P, ctypes.POINTER(I), ctypes.POINTER(I)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -146,6 +151,29 @@ def get_device() -> int:
     return _default_device
 
 
+_precision = os.environ.get("HS_PRECISION", "auto")
+if _precision not in PRECISIONS:
+    _precision = "auto"
+
+
+def set_precision(mode: str) -> None:
+    """Pixel-pass arithmetic of every plan: "auto" (default), "fp32", "fp64".
+
+    The reference computes in fp64 throughout.  "fp32" runs the fast fp32
+    pixel kernels (fp64 tables, folds and updates); "fp64" runs every pixel
+    product in fp64; "auto" picks fp64 when the smallest pixel set a call
+    projects over holds fewer than 512 pixels per spot (or n > 1024), where
+    WGS amplifies fp32 rounding past the parity tolerances."""
+    global _precision
+    if mode not in PRECISIONS:
+        raise InvalidParameterError(f"precision must be one of {sorted(PRECISIONS)}, got {mode!r}")
+    _precision = mode
+
+
+def get_precision() -> str:
+    return _precision
+
+
 class Plan:
     """One pupil's geometry resident on one device (hs_plan)."""
 
@@ -165,6 +193,7 @@ class Plan:
                                  ptr(axis), float(pupil.prism_coeff), float(pupil.lens_coeff),
                                  float(pupil.sum_amplitude), ctypes.byref(h)))
         self.handle = h
+        self._prec = None
         self._spots_key = None
         self.batch = 0
         self.n = 0
@@ -195,20 +224,34 @@ class Plan:
         self.batch, self.n = b, n
         self._spots_key = None
 
+    def _sync_precision(self) -> None:
+        if self._prec != _precision:
+            check(load().hs_set_precision(self.handle, PRECISIONS[_precision]))
+            self._prec = _precision
+
+    def last_precision(self) -> str:
+        """Arithmetic of the plan's last solve: "fp32" or "fp64"."""
+        mode, last = ctypes.c_int(), ctypes.c_int()
+        check(load().hs_get_precision(self.handle, ctypes.byref(mode), ctypes.byref(last)))
+        return "fp64" if last.value == PREC_FP64 else "fp32"
+
     # ---- kernels --------------------------------------------------------
     def superpose(self, amplitude, theta, start: int, stop: int) -> np.ndarray:
+        self._sync_precision()
         out = np.empty(stop - start, dtype=np.float64)
         a, t = f64(amplitude), f64(theta)
         check(load().hs_superpose(self.handle, ptr(a), ptr(t), start, stop, ptr(out)))
         return out
 
     def forward(self, phase, start: int, stop: int) -> np.ndarray:
+        self._sync_precision()
         ph = f64(phase)
         out = np.empty(2 * self.n, dtype=np.float64)
         check(load().hs_forward(self.handle, ptr(ph), start, stop, ptr(out)))
         return out[0::2] + 1j * out[1::2]
 
     def quality(self, phase):
+        self._sync_precision()
         ph = f64(phase)
         e, u = ctypes.c_double(), ctypes.c_double()
         inten = np.empty(self.n)
@@ -221,6 +264,7 @@ class Plan:
     # ---- solver ---------------------------------------------------------
     def solve(self, algorithm: int, iterations: int, subset: int, theta0,
               want_fields: bool = True, sync: bool = True, raster: bool = False) -> None:
+        self._sync_precision()
         th = f64(theta0)
         fn = load().hs_solve if sync else load().hs_solve_async
         flags = (WANT_FIELDS if want_fields else 0) | (WANT_RASTER if raster else 0)
@@ -269,6 +313,7 @@ class Plan:
         return e, u, inten, rel, fields[:, 0::2] + 1j * fields[:, 1::2]
 
     def probe(self, phase, points, batch: int = 1024) -> np.ndarray:
+        self._sync_precision()
         pts = f64(np.atleast_2d(points))
         out = np.empty(pts.shape[0], dtype=np.float64)
         try:
@@ -281,6 +326,7 @@ class Plan:
     # ---- row-sharded solve (distributed.solve_sharded) -----------------
     def shard_begin(self, algorithm: int, iterations: int, subset: int, theta0, rank: int,
                     world: int) -> None:
+        self._sync_precision()
         check(load().hs_shard_begin(self.handle, algorithm, iterations, subset,
                                     ptr(f64(theta0)), rank, world))
 

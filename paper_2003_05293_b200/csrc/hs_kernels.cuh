@@ -52,7 +52,8 @@ struct UpdArgs {
     int n, np;
     const double *a0;         // [B][n] target amplitudes
     double *w;                // [B][np] weights
-    float2 *coef;             // [B][np] coefficients for the next pass
+    float2 *coef;             // [B][np] coefficients for the next pass (fp32 passes)
+    double2 *coef64;          // [B][np] the same in fp64 (fp64 passes; coef unused)
     double *trace_w, *trace_m;  // [B][iters][n]
     int iter, iters;
     int32_t *status, *degen, *qstatus;  // [B]
@@ -67,7 +68,8 @@ struct FoldArgs {
     int32_t chunk_base;       // first chunk of this launch (row-sharded passes)
     int32_t chunk_end;        // one past the last chunk of this launch
     int32_t np;
-    float2 *partials;         // [B][part_stride]: [chunk][np]
+    float2 *partials;         // [B][part_stride]: [chunk][np] (fp32 passes)
+    double2 *partials64;      // the same layout in fp64 (fp64 passes; partials unused)
     int64_t part_stride;
     double2 *gpart;           // [B][gpart_stride]: [group][np]
     int64_t gpart_stride;
@@ -184,20 +186,23 @@ __device__ __forceinline__ unsigned char hs_gray_linear(double p)
     return (unsigned char)(((long long)g) & 255);
 }
 
+// coef = a e^{i wrap(theta)} (kernels.py:206-208); fp32 (coef) or fp64 (coef64)
 __device__ __forceinline__ void hs_seed_one(int b, int k, int n, int np, const double *amp,
-                                            const double *theta, float2 *coef, double *w)
+                                            const double *theta, float2 *coef, double *w,
+                                            double2 *coef64 = nullptr)
 {
-    float2 c = make_float2(0.f, 0.f);
+    double2 c = make_double2(0.0, 0.0);
     double wk = 0.0;
     if (k < n) {
         const double th = hs_wrap(theta[(int64_t)b * n + k]);
         const double am = amp[(int64_t)b * n + k];
         double s, co;
         sincos(th, &s, &co);
-        c = make_float2((float)(am * co), (float)(am * s));
+        c = make_double2(am * co, am * s);
         wk = 1.0;
     }
-    coef[(int64_t)b * np + k] = c;
+    if (coef64) coef64[(int64_t)b * np + k] = c;
+    else coef[(int64_t)b * np + k] = make_float2((float)c.x, (float)c.y);
     if (w) w[(int64_t)b * np + k] = wk;
 }
 
@@ -238,9 +243,10 @@ static __global__ void hs_tables_kernel(int side, int np, int n, const double *_
 }
 
 static __global__ void hs_seed_kernel(int n, int np, const double *amp, const double *theta, float2 *coef,
-                               double *w)
+                               double *w, double2 *coef64 = nullptr)
 {
-    for (int k = threadIdx.x; k < np; k += blockDim.x) hs_seed_one(blockIdx.x, k, n, np, amp, theta, coef, w);
+    for (int k = threadIdx.x; k < np; k += blockDim.x)
+        hs_seed_one(blockIdx.x, k, n, np, amp, theta, coef, w, coef64);
 }
 
 // ---------------------------------------------------------------------------
@@ -367,7 +373,8 @@ __device__ __forceinline__ void hs_update(const UpdArgs &a, int b, double2 *E, d
         }
         double s, co;
         sincos(th, &s, &co);
-        a.coef[(int64_t)b * np + k] = make_float2((float)(am * co), (float)(am * s));
+        if (a.coef64) a.coef64[(int64_t)b * np + k] = make_double2(am * co, am * s);
+        else a.coef[(int64_t)b * np + k] = make_float2((float)(am * co), (float)(am * s));
     }
 }
 
@@ -395,16 +402,29 @@ __device__ __forceinline__ void hs_fold(const FoldArgs &a, int pat, int chunk, c
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    const float2 *part = a.partials + (int64_t)pat * a.part_stride;
     double2 *gp = a.gpart + (int64_t)pat * a.gpart_stride;
-    for (int k = tid; k < np; k += kThreads) {
-        double sx = 0.0, sy = 0.0;
-        for (int c = c0; c < c1; ++c) {
-            const float2 v = __ldcg(part + (int64_t)c * np + k);
-            sx += (double)v.x;
-            sy += (double)v.y;
+    if (a.partials64) {
+        const double2 *part = a.partials64 + (int64_t)pat * a.part_stride;
+        for (int k = tid; k < np; k += kThreads) {
+            double sx = 0.0, sy = 0.0;
+            for (int c = c0; c < c1; ++c) {
+                const double2 v = __ldcg(part + (int64_t)c * np + k);
+                sx += v.x;
+                sy += v.y;
+            }
+            gp[(int64_t)grp * np + k] = make_double2(sx, sy);
         }
-        gp[(int64_t)grp * np + k] = make_double2(sx, sy);
+    } else {
+        const float2 *part = a.partials + (int64_t)pat * a.part_stride;
+        for (int k = tid; k < np; k += kThreads) {
+            double sx = 0.0, sy = 0.0;
+            for (int c = c0; c < c1; ++c) {
+                const float2 v = __ldcg(part + (int64_t)c * np + k);
+                sx += (double)v.x;
+                sy += (double)v.y;
+            }
+            gp[(int64_t)grp * np + k] = make_double2(sx, sy);
+        }
     }
     if (tid == 0) a.grp_cnt[(int64_t)pat * a.cnt_stride + grp] = 0;
     __threadfence();

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <map>
 #include <memory>
 #include <string>
@@ -27,6 +28,7 @@
 #include "hs_xchg.cuh"
 #include "hs_slab.cuh"
 #include "hs_umma.cuh"
+#include "hs_f64.cuh"
 
 using namespace hs;
 
@@ -54,6 +56,12 @@ int fail(int code, const char *fmt, ...)
 
 constexpr int kColBlock = 64;  // dense layout: columns per CTA chunk
 constexpr int kSplitBatch = 16;  // batches >= this record two graph branches (record_solve)
+constexpr int kMaxSpots32 = 1024;   // largest n of the fp32 pixel kernels (G = 32 lanes x NL = 32)
+constexpr int kMaxSpots = 4096;     // largest n overall (fp64 passes: the fold keeps 32 B per spot in smem)
+// precision "auto": fp64 passes when the smallest pixel set a solve projects
+// over holds fewer than this many pixels per spot
+constexpr int64_t kAutoPixelsPerSpot = 512;
+constexpr size_t kPass64SmemMax = 160 * 1024;
 
 struct DevList {
     int32_t *rc = nullptr;
@@ -98,6 +106,14 @@ Config pick_config(int n)
 {
     Config c{};
     const int choices[] = {4, 8, 10, 12, 14, 16, 32};
+    if (n > kMaxSpots32) {  // fp64 passes only (NL = 0 marks "no fp32 kernel")
+        c.G = 32;
+        c.NL = 0;
+        c.np = 32 * ((n + 31) / 32);
+        c.ns = 0;
+        c.spw = 1;
+        return c;
+    }
     if (n <= 128) {
         c.np = 16 * ((n + 15) / 16);
         c.ns = c.np / 16;
@@ -155,7 +171,7 @@ struct hs_plan {
     int32_t *d_utiles = nullptr;          // non-empty 128x64 tiles of the tcgen05 full pass
     int32_t nutiles = 0;
     bool umma_enabled = true;             // HS_UMMA=0: FFMA tiles (hs_tile) for every n
-    int umma_max_n = 128;                 // largest n on the tensor cores (HS_UMMA_MAXN, experiments)
+    int umma_max_n = kMaxSpots32;         // largest n on the tensor cores (HS_UMMA_MAXN, experiments)
     int num_sms = 148;
     bool pdl = false;                     // next pass launch: programmatic dependent launch
     int view0 = 0;                        // first pattern of the sub-batch being recorded
@@ -197,6 +213,15 @@ struct hs_plan {
     cudaEvent_t solved[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
     double *d_trace_w = nullptr, *d_trace_m = nullptr;
     int64_t trace_cap = 0;
+    // fp64 passes (hs_f64.cuh): precision mode, buffers allocated on first use
+    int precision_mode = HS_PREC_AUTO;    // hs_set_precision / HS_PRECISION
+    bool use64 = false;                   // passes being recorded / launched run in fp64
+    int last_precision = HS_PREC_FP32;    // precision of the last solve
+    double *d_amp64 = nullptr;            // [m] storage-order amplitude
+    double2 *d_gx64 = nullptr, *d_gy64 = nullptr;  // [B][side][np] (one allocation)
+    double2 *d_coef64 = nullptr;          // [B][np]
+    double2 *d_part64 = nullptr;          // [B][part_stride]
+    bool tables64_valid = false;
 
     int last_alg = -1, last_iters = 0, last_flags = 0;
     // row-sharded solve state (hs_shard_*)
@@ -485,6 +510,7 @@ void free_graphs(hs_plan *p)
 void free_fold(hs_plan *p)
 {
     dfree(p->d_part);
+    dfree(p->d_part64);
     dfree(p->d_gpart);
     dfree(p->d_grp_cnt);
     dfree(p->d_pat_cnt);
@@ -496,6 +522,7 @@ void free_batch(hs_plan *p)
     dfree(p->d_x); dfree(p->d_y); dfree(p->d_z); dfree(p->d_a0);
     dfree(p->d_theta); dfree(p->d_amp_in);
     dfree(p->d_gx); p->d_gy = nullptr; dfree(p->d_w); dfree(p->d_coef);
+    dfree(p->d_gx64); p->d_gy64 = nullptr; dfree(p->d_coef64); p->tables64_valid = false;
     dfree(p->d_gyp); p->gyp_stride = 0;
     dfree(p->d_status); dfree(p->d_degen); dfree(p->d_qstatus);
     dfree(p->d_fields); dfree(p->d_e); dfree(p->d_u); dfree(p->d_inten); dfree(p->d_rel);
@@ -529,7 +556,7 @@ int ensure_batch(hs_plan *p, int batch, int n)
         free_batch(p);
         return rc;
     }
-    if (p->umma_enabled) {
+    if (p->umma_enabled && cfg.NL > 0) {
         p->gyp_stride = hs_umma_plane_floats(p->side, cfg.np);
         if ((rc = dalloc(&p->d_gyp, (size_t)B * p->gyp_stride))) {
             free_batch(p);
@@ -579,6 +606,32 @@ int ensure_trace(hs_plan *p, int iters)
     return HS_OK;
 }
 
+// fp64 pass buffers (tables, coefficients, partials), allocated on first use.
+int ensure64(hs_plan *p)
+{
+    int rc;
+    if (!p->d_gx64) {
+        const size_t tab = (size_t)p->cap_batch * p->side * p->cap_np;
+        if ((rc = dalloc(&p->d_gx64, 2 * tab)) || (rc = dalloc(&p->d_coef64, (size_t)p->cap_batch * p->cap_np)))
+            return rc;
+        p->d_gy64 = p->d_gx64 + tab;
+        p->tables64_valid = false;
+    }
+    if (!p->d_part64 && (rc = dalloc(&p->d_part64, (size_t)p->cap_batch * p->part_stride))) return rc;
+    return HS_OK;
+}
+
+// Does a call projecting over at least `min_pixels` pixels per pattern run
+// the fp64 passes?  (HS_PREC_AUTO rule: fewer than kAutoPixelsPerSpot pixels
+// per spot, or more spots than the fp32 kernels carry.)
+bool want64(const hs_plan *p, int64_t min_pixels)
+{
+    if (p->cfg.NL == 0) return true;
+    if (p->precision_mode == HS_PREC_FP64) return true;
+    if (p->precision_mode == HS_PREC_FP32) return false;
+    return min_pixels < kAutoPixelsPerSpot * (int64_t)p->n;
+}
+
 UpdArgs upd_args(hs_plan *p, int act)
 {
     UpdArgs u;
@@ -590,7 +643,8 @@ UpdArgs upd_args(hs_plan *p, int act)
     const int64_t b0 = p->view0, n = p->n, np = p->cfg.np;
     u.a0 = p->d_a0 + b0 * n;
     u.w = p->d_w + b0 * np;
-    u.coef = p->d_coef + b0 * np;
+    if (p->use64) u.coef64 = p->d_coef64 + b0 * np;
+    else u.coef = p->d_coef + b0 * np;
     u.trace_w = p->d_trace_w;
     u.trace_m = p->d_trace_m;
     u.iters = 1;
@@ -607,7 +661,7 @@ UpdArgs upd_args(hs_plan *p, int act)
 }
 
 // Full-range tile list of the current configuration: the tcgen05 pass's
-// 128 x 64 tiles (hs_umma) for 32 < n <= 128 unless HS_UMMA=0, else the FFMA 64 x 64 tiles.
+// 128 x 64 tiles (hs_umma) for 32 < n <= 1024 unless HS_UMMA=0, else the FFMA 64 x 64 tiles.
 struct TileSet {
     const int32_t *d;
     int32_t n;
@@ -619,10 +673,11 @@ TileSet tile_set(const hs_plan *p)
     // few spots: the per-tile fixed costs of the tensor-core pass outweigh its
     // MMA speed (config 1, N = 10: 0.181 vs 0.157 ms per solve).  Many spots:
     // the 3-term tf32 products (~2^-21 relative each, against 2^-24 for an
-    // FFMA) leave the magnitudes ~10-20x further from the oracle; up to
-    // n = 128 that is <= 4e-6 (tolerance 1e-4), at n = 200 / 600 the weights
-    // drift past 1e-4 over the iterations where the FFMA tiles stay inside
-    // (tests/test_gpu_spot_chunks.py), so larger n run the FFMA tiles.
+    // FFMA) leave the magnitudes ~5-10x further from the oracle than the
+    // FFMA tiles'.  Where the fp32 passes run at all (>= 512 pixels per spot
+    // under precision "auto"; fewer run the fp64 passes) that is <= 4e-6 at
+    // 30 iterations (config 4: 4.1e-6 trace, 7.6e-6 intensities; tolerance
+    // 1e-4; tools/accuracy_probe.py), so every n <= 1024 runs here.
     if (p->umma_enabled && p->n > 32 && p->n <= p->umma_max_n && p->d_gyp &&
         p->gyp_stride >= hs_umma_plane_floats(p->side, p->cfg.np))
         return {p->d_utiles, p->nutiles, true};
@@ -632,6 +687,13 @@ TileSet tile_set(const hs_plan *p)
 int launch_tables(hs_plan *p, bool seed, bool with_prep = true)
 {
     dim3 grid(p->side, p->batch);
+    if (p->use64) {
+        hs_tables64_kernel<<<grid, 128, 0, p->stream>>>(p->side, p->cfg.np, p->n, p->d_axis, p->c1, p->c2, p->d_x,
+                                                        p->d_y, p->d_z, p->d_gx64, p->d_gy64, p->d_a0,
+                                                        seed ? p->d_theta : nullptr, p->d_coef64, p->d_w);
+        CUDA_TRY(cudaGetLastError());
+        return HS_OK;
+    }
     hs_tables_kernel<<<grid, 128, 0, p->stream>>>(p->side, p->cfg.np, p->n, p->d_axis, p->c1, p->c2, p->d_x,
                                                   p->d_y, p->d_z, p->d_gx, p->d_gy, p->d_a0,
                                                   seed ? p->d_theta : nullptr, p->d_coef, p->d_w);
@@ -650,12 +712,14 @@ int launch_tables(hs_plan *p, bool seed, bool with_prep = true)
 FoldArgs fold_args(hs_plan *p, int32_t nchunks, const UpdArgs &u, int32_t lo = 0, int32_t hi = -1)
 {
     FoldArgs f;
+    memset(&f, 0, sizeof f);
     f.nchunks = nchunks;
     f.chunk_base = lo;
     f.chunk_end = hi < 0 ? nchunks : hi;
     f.np = p->cfg.np;
     const int64_t b0 = p->view0;
-    f.partials = p->d_part + b0 * p->part_stride;
+    if (p->use64) f.partials64 = p->d_part64 + b0 * p->part_stride;
+    else f.partials = p->d_part + b0 * p->part_stride;
     f.part_stride = p->part_stride;
     f.gpart = p->d_gpart + b0 * p->gpart_stride;
     f.gpart_stride = p->gpart_stride;
@@ -832,17 +896,62 @@ int reset_status(hs_plan *p)
 
 int ensure_tables(hs_plan *p)
 {
+    int rc;
+    if (p->use64) {
+        if ((rc = ensure64(p))) return rc;
+        if (p->tables64_valid) return HS_OK;
+        if ((rc = launch_tables(p, false))) return rc;
+        p->tables64_valid = true;
+        return HS_OK;
+    }
     if (p->tables_valid) return HS_OK;
-    int rc = launch_tables(p, false);
-    if (rc) return rc;
+    if ((rc = launch_tables(p, false))) return rc;
     p->tables_valid = true;
     return HS_OK;
 }
 
+// fp64 pass over storage pixels [start, start + count) of every pattern of
+// the current view (hs_pass64_kernel): chunk length ~count / kTargetChunks,
+// a multiple of 8 pixels, at most kMaxChunk -- never more chunks than the
+// fold buffers hold.
+int launch_pass64(hs_plan *p, int mode, int64_t start, int64_t count, const double *phase_in, double *phase_out,
+                  int64_t phase_stride, const UpdArgs &u, unsigned char *raster = nullptr)
+{
+    if (count == 0) return HS_OK;
+    int64_t per = (count + kTargetChunks - 1) / kTargetChunks;
+    per = std::min<int64_t>(std::max<int64_t>((per + 7) / 8 * 8, 8), kMaxChunk);
+    const int32_t nchunks = (int32_t)((count + per - 1) / per);
+    if (nchunks > p->cap_chunks) return fail(HS_ECUDA, "fold buffers too small (%d chunks)", nchunks);
+    Pass64Args a;
+    memset(&a, 0, sizeof a);
+    a.rc = p->storage.rc;
+    a.amp = p->d_amp64;
+    a.start = start;
+    a.count = count;
+    a.chunk_len = (int32_t)per;
+    a.n = p->n;
+    a.np = p->cfg.np;
+    a.tab_stride = (int64_t)p->side * p->cfg.np;
+    a.gx = p->d_gx64 + p->view0 * a.tab_stride;
+    a.gy = p->d_gy64 + p->view0 * a.tab_stride;
+    a.coef = p->d_coef64 + (int64_t)p->view0 * p->cfg.np;
+    a.phase_in = phase_in ? phase_in + p->view0 * phase_stride : nullptr;
+    a.phase_out = phase_out ? phase_out + p->view0 * phase_stride : nullptr;
+    a.phase_stride = phase_stride;
+    a.raster = raster ? raster + (int64_t)p->view0 * p->side * p->side : nullptr;
+    a.side = p->side;
+    a.f = fold_args(p, nchunks, u);
+    const size_t smem = hs_pass64_smem_bytes(p->cfg.np, (int)per);
+    return launch_pass_kernel(p, hs_select_pass64(mode), dim3(nchunks, p->batch), dim3(kP64Threads), smem, a);
+}
+
 // The passes of one sub-batch (patterns view0 .. view0 + batch - 1) on the
 // current p->stream.
+int record_passes64(hs_plan *p, int alg, int iters, int64_t subset, int flags, double *out);
+
 int record_passes(hs_plan *p, int alg, int iters, int64_t subset, int flags, double *out)
 {
+    if (p->use64) return record_passes64(p, alg, iters, subset, flags, out);
     int rc;
     const bool want_fields = (flags & HS_WANT_FIELDS) != 0;
     const int64_t m = p->m;
@@ -889,6 +998,45 @@ int record_passes(hs_plan *p, int alg, int iters, int64_t subset, int flags, dou
     return HS_OK;
 }
 
+// The fp64 schedule: the same passes as record_passes over storage-order
+// ranges (the windows of the schedule are contiguous storage ranges, so no
+// lists are needed).
+int record_passes64(hs_plan *p, int alg, int iters, int64_t subset, int flags, double *out)
+{
+    int rc;
+    const bool want_fields = (flags & HS_WANT_FIELDS) != 0;
+    const int64_t m = p->m;
+    const int final_mode = want_fields ? (PM_BWD | PM_FWD | PM_WRITE) : (PM_BWD | PM_WRITE);
+    const UpdArgs fin = upd_args(p, want_fields ? ACT_FINAL : ACT_NONE);
+    unsigned char *raster = (flags & HS_WANT_RASTER) ? p->d_raster : nullptr;
+    if (alg == HS_ALG_RS) return launch_pass64(p, final_mode, 0, m, nullptr, out, m, fin, raster);
+    const int cs = (subset < m) ? std::max(0, iters - 2) : 0;
+    const int64_t half = std::max<int64_t>(1, subset / 2);
+    for (int j = 0; j <= iters; ++j) {
+        int64_t off = 0, cnt = m;
+        if (j == 0 ? cs > 0 : j <= cs) {
+            off = (j == 0) ? 0 : ((int64_t)(j - 1) * half) % (m - subset + 1);
+            cnt = subset;
+        }
+        UpdArgs u = fin;
+        int mode = final_mode;
+        if (j < iters) {
+            u = upd_args(p, ACT_STEP);
+            u.iter = j;
+            u.iters = iters;
+            u.trace_w += (int64_t)p->view0 * iters * p->n;
+            u.trace_m += (int64_t)p->view0 * iters * p->n;
+            mode = PM_BWD | PM_FWD;
+        }
+        p->pdl = (j > 0);
+        rc = launch_pass64(p, mode, off, cnt, nullptr, j == iters ? out : nullptr, m, u,
+                           j == iters ? raster : nullptr);
+        p->pdl = false;
+        if (rc) return rc;
+    }
+    return HS_OK;
+}
+
 // The solve schedule (solvers.py:192-235), fused: pass 0 superposes coef_0
 // over read_1 and projects it; the fold of pass j applies iteration j+1's
 // update (trace record j+1, coef_{j+1}); pass j >= 1 superposes coef_j over
@@ -907,7 +1055,7 @@ int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags, doub
     if ((rc = launch_tables(p, true, false))) return rc;
     // the tcgen05 operand planes are first read by the full passes at the end
     // of the schedule: prepare them on a side stream beside the window passes
-    if (p->d_gyp && tile_set(p).umma) {
+    if (!p->use64 && p->d_gyp && tile_set(p).umma) {
         CUDA_TRY(cudaEventRecord(p->fork_ev, p->stream));
         CUDA_TRY(cudaStreamWaitEvent(p->stream3, p->fork_ev, 0));
         dim3 pg((unsigned)((p->side + kUR - 1) / kUR * (p->cfg.np / kUF) +
@@ -963,6 +1111,14 @@ int check_device(hs_plan *p)
     return HS_OK;
 }
 
+// Compute entry points: forced fp32 cannot carry more than kMaxSpots32 spots.
+int check_prec(hs_plan *p)
+{
+    if (p->cfg.NL == 0 && p->precision_mode == HS_PREC_FP32)
+        return fail(HS_EINVAL, "precision fp32 carries at most %d spots (n = %d)", kMaxSpots32, p->n);
+    return HS_OK;
+}
+
 int sync_and_check(hs_plan *p)
 {
     CUDA_TRY(cudaStreamSynchronize(p->stream));
@@ -989,9 +1145,24 @@ int hs_device_count(int *count)
     return HS_OK;
 }
 
-int hs_max_spots(void) { return 1024; }
+int hs_max_spots(void) { return kMaxSpots; }
 
 int hs_padded_spots(hs_plan *p) { return p->cfg.np; }
+
+int hs_set_precision(hs_plan *p, int mode)
+{
+    if (mode != HS_PREC_AUTO && mode != HS_PREC_FP32 && mode != HS_PREC_FP64)
+        return fail(HS_EINVAL, "precision mode %d invalid", mode);
+    p->precision_mode = mode;
+    return HS_OK;
+}
+
+int hs_get_precision(hs_plan *p, int *mode, int *last_solve)
+{
+    if (mode) *mode = p->precision_mode;
+    if (last_solve) *last_solve = p->last_precision;
+    return HS_OK;
+}
 
 int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const int64_t *cols,
                    const double *amplitude, const double *axis, double prism, double lens,
@@ -1038,8 +1209,16 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
         p->row_hi[r] = std::max(p->row_hi[r], c + 1);
     }
     int rc;
-    if ((rc = dalloc(&p->d_axis, side))) return rc;
+    if ((rc = dalloc(&p->d_axis, side)) || (rc = dalloc(&p->d_amp64, m))) return rc;
     CUDA_TRY(cudaMemcpy(p->d_axis, axis, sizeof(double) * side, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(p->d_amp64, amplitude, sizeof(double) * m, cudaMemcpyHostToDevice));
+    if (const char *env = getenv("HS_PRECISION")) {
+        if (!strcmp(env, "fp32")) p->precision_mode = HS_PREC_FP32;
+        else if (!strcmp(env, "fp64")) p->precision_mode = HS_PREC_FP64;
+    }
+    for (int mode : std::initializer_list<int>{PM_BWD | PM_WRITE, PM_FWD, PM_BWD | PM_FWD, PM_BWD | PM_FWD | PM_WRITE})
+        CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_pass64(mode),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPass64SmemMax));
     if ((rc = build_storage(p.get()))) return rc;
     {
         const size_t cells = (size_t)side * side;
@@ -1125,6 +1304,7 @@ void hs_plan_destroy(hs_plan *p)
     for (auto &kv : p->dense) free_list(kv.second);
     for (auto &kv : p->windows) free_list(kv.second);
     dfree(p->d_axis);
+    dfree(p->d_amp64);
     dfree(p->d_amp_img);
     dfree(p->d_idx_img);
     dfree(p->d_tiles);
@@ -1171,6 +1351,7 @@ int hs_set_spots(hs_plan *p, int batch, int n, const double *x, const double *y,
     CUDA_TRY(cudaMemcpyAsync(p->d_z, z, bytes, cudaMemcpyHostToDevice, p->stream));
     CUDA_TRY(cudaMemcpyAsync(p->d_a0, a0, bytes, cudaMemcpyHostToDevice, p->stream));
     p->tables_valid = false;
+    p->tables64_valid = false;
     return HS_OK;
 }
 
@@ -1182,6 +1363,18 @@ static int check_range(hs_plan *p, int64_t start, int64_t stop)
                     (long long)p->m);
     return HS_OK;
 }
+
+// API calls: precision of the passes of this call (want64 over the whole
+// pupil), reset when the call returns.
+struct Use64 {
+    hs_plan *p;
+    Use64(hs_plan *pl, int64_t pixels) : p(pl)
+    {
+        p->use64 = want64(p, pixels);
+        if (p->use64 && ensure64(p)) p->use64 = false;  // allocation failure surfaces in ensure_tables
+    }
+    ~Use64() { p->use64 = false; }
+};
 
 // API passes act on pattern 0 only.
 struct OnePattern {
@@ -1195,19 +1388,24 @@ int hs_superpose(hs_plan *p, const double *amplitude, const double *theta, int64
                  double *out)
 {
     int rc;
-    if ((rc = check_range(p, start, stop)) || (rc = check_device(p)) || (rc = ensure_tables(p)) ||
-        (rc = reset_status(p)))
-        return rc;
+    if ((rc = check_range(p, start, stop)) || (rc = check_device(p)) || (rc = check_prec(p))) return rc;
+    Use64 prec(p, p->m);
+    if ((rc = ensure_tables(p)) || (rc = reset_status(p))) return rc;
     if (stop == start) return HS_OK;
     const size_t bytes = sizeof(double) * p->n;
     CUDA_TRY(cudaMemcpyAsync(p->d_amp_in, amplitude, bytes, cudaMemcpyHostToDevice, p->stream));
     CUDA_TRY(cudaMemcpyAsync(p->d_theta, theta, bytes, cudaMemcpyHostToDevice, p->stream));
     {
         OnePattern one(p);
-        hs_seed_kernel<<<1, 256, 0, p->stream>>>(p->n, p->cfg.np, p->d_amp_in, p->d_theta, p->d_coef, nullptr);
+        hs_seed_kernel<<<1, 256, 0, p->stream>>>(p->n, p->cfg.np, p->d_amp_in, p->d_theta, p->d_coef, nullptr,
+                                                 p->use64 ? p->d_coef64 : nullptr);
         CUDA_TRY(cudaGetLastError());
-        rc = launch_pass(p, PM_BWD | PM_WRITE, p->storage, start, stop - start, 0, nullptr, p->d_phase, 0,
-                         upd_args(p, ACT_NONE));
+        if (p->use64)
+            rc = launch_pass64(p, PM_BWD | PM_WRITE, start, stop - start, nullptr, p->d_phase - start, 0,
+                               upd_args(p, ACT_NONE));
+        else
+            rc = launch_pass(p, PM_BWD | PM_WRITE, p->storage, start, stop - start, 0, nullptr, p->d_phase, 0,
+                             upd_args(p, ACT_NONE));
         if (rc) return rc;
     }
     CUDA_TRY(cudaMemcpyAsync(out, p->d_phase, sizeof(double) * (stop - start), cudaMemcpyDeviceToHost, p->stream));
@@ -1217,9 +1415,9 @@ int hs_superpose(hs_plan *p, const double *amplitude, const double *theta, int64
 int hs_forward(hs_plan *p, const double *phase, int64_t start, int64_t stop, double *fields)
 {
     int rc;
-    if ((rc = check_range(p, start, stop)) || (rc = check_device(p)) || (rc = ensure_tables(p)) ||
-        (rc = reset_status(p)))
-        return rc;
+    if ((rc = check_range(p, start, stop)) || (rc = check_device(p)) || (rc = check_prec(p))) return rc;
+    Use64 prec(p, p->m);
+    if ((rc = ensure_tables(p)) || (rc = reset_status(p))) return rc;
     if (stop == start) {  // kernels.py:234-235
         memset(fields, 0, sizeof(double) * 2 * p->n);
         return HS_OK;
@@ -1227,8 +1425,11 @@ int hs_forward(hs_plan *p, const double *phase, int64_t start, int64_t stop, dou
     CUDA_TRY(cudaMemcpyAsync(p->d_phase, phase, sizeof(double) * p->m, cudaMemcpyHostToDevice, p->stream));
     {
         OnePattern one(p);
-        rc = launch_pass(p, PM_FWD, p->storage, start, stop - start, start, p->d_phase, nullptr, 0,
-                         upd_args(p, ACT_FIELDS));
+        if (p->use64)
+            rc = launch_pass64(p, PM_FWD, start, stop - start, p->d_phase, nullptr, 0, upd_args(p, ACT_FIELDS));
+        else
+            rc = launch_pass(p, PM_FWD, p->storage, start, stop - start, start, p->d_phase, nullptr, 0,
+                             upd_args(p, ACT_FIELDS));
         if (rc) return rc;
     }
     CUDA_TRY(cudaMemcpyAsync(fields, p->d_fields, sizeof(double) * 2 * p->n, cudaMemcpyDeviceToHost, p->stream));
@@ -1240,15 +1441,18 @@ int hs_quality(hs_plan *p, const double *phase, double *e, double *u, double *in
 {
     if (!(p->sum_amp > 0.0)) return fail(HS_EZEROILLUM, "pupil carries no illumination");
     int rc;
-    if ((rc = check_range(p, 0, p->m)) || (rc = check_device(p)) || (rc = ensure_tables(p)) ||
-        (rc = reset_status(p)))
-        return rc;
+    if ((rc = check_range(p, 0, p->m)) || (rc = check_device(p)) || (rc = check_prec(p))) return rc;
+    Use64 prec(p, p->m);
+    if ((rc = ensure_tables(p)) || (rc = reset_status(p))) return rc;
     const DevList *dense;
     if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
     CUDA_TRY(cudaMemcpyAsync(p->d_phase, phase, sizeof(double) * p->m, cudaMemcpyHostToDevice, p->stream));
     {
         OnePattern one(p);
-        rc = launch_pass(p, PM_FWD, *dense, 0, dense->count, 0, p->d_phase, nullptr, 0, upd_args(p, ACT_FINAL));
+        if (p->use64)
+            rc = launch_pass64(p, PM_FWD, 0, p->m, p->d_phase, nullptr, 0, upd_args(p, ACT_FINAL));
+        else
+            rc = launch_pass(p, PM_FWD, *dense, 0, dense->count, 0, p->d_phase, nullptr, 0, upd_args(p, ACT_FINAL));
         if (rc) return rc;
     }
     int32_t qs = 0;
@@ -1283,16 +1487,20 @@ int hs_probe(hs_plan *p, const double *phase, int64_t npts, const double *xyz, i
             y[k] = xyz[(lo + k) * 3 + 1];
             z[k] = xyz[(lo + k) * 3 + 2];
         }
-        if ((rc = hs_set_spots(p, 1, n, x.data(), y.data(), z.data(), a.data())) || (rc = ensure_tables(p)) ||
-            (rc = reset_status(p)))
-            return rc;
+        if ((rc = hs_set_spots(p, 1, n, x.data(), y.data(), z.data(), a.data())) || (rc = check_prec(p))) return rc;
+        Use64 prec(p, p->m);
+        if ((rc = ensure_tables(p)) || (rc = reset_status(p))) return rc;
         if (!uploaded) {
             CUDA_TRY(cudaMemcpyAsync(p->d_phase, phase, sizeof(double) * p->m, cudaMemcpyHostToDevice, p->stream));
             uploaded = true;
         }
-        const DevList *dense;
-        if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
-        rc = launch_pass(p, PM_FWD, *dense, 0, dense->count, 0, p->d_phase, nullptr, 0, upd_args(p, ACT_FINAL));
+        if (p->use64) {
+            rc = launch_pass64(p, PM_FWD, 0, p->m, p->d_phase, nullptr, 0, upd_args(p, ACT_FINAL));
+        } else {
+            const DevList *dense;
+            if ((rc = get_dense(p, p->cfg.spw, &dense))) return rc;
+            rc = launch_pass(p, PM_FWD, *dense, 0, dense->count, 0, p->d_phase, nullptr, 0, upd_args(p, ACT_FINAL));
+        }
         if (rc) return rc;
         CUDA_TRY(cudaMemcpyAsync(out + lo, p->d_inten, sizeof(double) * n, cudaMemcpyDeviceToHost, p->stream));
     }
@@ -1322,11 +1530,19 @@ static int solve_into(hs_plan *p, int alg, int iters, int64_t subset, const doub
     }
     if ((flags & HS_WANT_FIELDS) && !(p->sum_amp > 0.0)) return fail(HS_EZEROILLUM, "pupil carries no illumination");
     int rc;
-    if ((rc = check_device(p)) || (rc = ensure_trace(p, iters))) return rc;
+    if ((rc = check_device(p)) || (rc = check_prec(p)) || (rc = ensure_trace(p, iters))) return rc;
+    // precision of this solve: the smallest pixel set it projects over
+    const bool windows = alg != HS_ALG_RS && subset < p->m && iters > 2;
+    p->use64 = want64(p, windows ? subset : p->m);
+    struct Reset64 {
+        hs_plan *p;
+        ~Reset64() { p->use64 = false; }
+    } reset64{p};
+    if (p->use64 && (rc = ensure64(p))) return rc;
     // host-side list building happens outside graph capture
     const DevList *l;
-    if ((rc = get_dense(p, p->cfg.spw, &l))) return rc;
-    if (alg != HS_ALG_RS && subset < p->m && iters > 2) {
+    if (!p->use64 && (rc = get_dense(p, p->cfg.spw, &l))) return rc;
+    if (!p->use64 && windows) {
         const int64_t half = std::max<int64_t>(1, subset / 2);
         for (int j = 0; j <= iters - 2; ++j) {
             const int64_t off = j == 0 ? 0 : ((int64_t)(j - 1) * half) % (p->m - subset + 1);
@@ -1335,7 +1551,7 @@ static int solve_into(hs_plan *p, int alg, int iters, int64_t subset, const doub
     }
     const size_t bytes = sizeof(double) * (size_t)p->batch * p->n;
     CUDA_TRY(cudaMemcpyAsync(p->d_theta, theta0, bytes, cudaMemcpyHostToDevice, p->stream));
-    auto key = std::make_tuple(alg, iters, subset, flags | (slot << 8), p->batch, p->n);
+    auto key = std::make_tuple(alg, iters, subset, flags | (slot << 8) | ((int)p->use64 << 12), p->batch, p->n);
     auto it = p->graphs.find(key);
     if (it == p->graphs.end()) {
         cudaGraph_t graph;
@@ -1352,14 +1568,16 @@ static int solve_into(hs_plan *p, int alg, int iters, int64_t subset, const doub
     }
     CUDA_TRY(cudaGraphLaunch(it->second, p->stream));
     p->out_slot = slot;
-    p->tables_valid = true;
+    if (p->use64) p->tables64_valid = true;
+    else p->tables_valid = true;
+    p->last_precision = p->use64 ? HS_PREC_FP64 : HS_PREC_FP32;
     p->last_alg = alg;
     p->last_iters = iters;
     p->last_flags = flags;
     {   // tables(+seed) [+ tcgen05 operand planes] + passes, per graph branch
         static const bool no_split = getenv("HS_SPLIT") && atoi(getenv("HS_SPLIT")) == 0;
         const int branches = (p->batch >= kSplitBatch && !no_split) ? 2 : 1;
-        const int prep = (p->d_gyp && tile_set(p).umma) ? 1 : 0;
+        const int prep = (!p->use64 && p->d_gyp && tile_set(p).umma) ? 1 : 0;
         p->last_launches = 1 + prep + (int64_t)branches * ((alg == HS_ALG_RS) ? 1 : iters + 1);
     }
     return HS_OK;
@@ -1518,6 +1736,8 @@ int hs_shard_begin(hs_plan *p, int alg, int iters, int64_t subset, const double 
         if (subset < 1 || subset > p->m) return fail(HS_EINVAL, "subset size outside 1..M");
     }
     if (!(p->sum_amp > 0.0)) return fail(HS_EZEROILLUM, "pupil carries no illumination");
+    if (p->cfg.NL == 0 || p->precision_mode == HS_PREC_FP64)
+        return fail(HS_EINVAL, "the row-sharded solve runs the fp32 passes only (n <= %d)", kMaxSpots32);
     int rc;
     if ((rc = check_device(p)) || (rc = ensure_trace(p, iters))) return rc;
     auto &sh = p->shard;

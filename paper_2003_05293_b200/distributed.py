@@ -95,7 +95,11 @@ def solve_sharded(pupil, spots, config, rank: int, world: int, all_gather, devic
     complex128 per pass) through the host.  Either
     way the phase slabs are gathered at the end, and the result
     ``(Hologram, SolverTrace)`` is identical on every rank and bitwise equal
-    to :func:`paper_2003_05293_b200.solve` on one GPU.
+    to :func:`paper_2003_05293_b200.solve` on one GPU with precision "fp32":
+    the sharded passes are the fp32 kernels (n <= 1024; precision "fp64"
+    raises InvalidParameterError).  Row sharding pays for large, well-
+    conditioned problems (config 4: 1042 pixels per spot), which precision
+    "auto" runs in fp32 on one GPU as well.
     """
     import time
 

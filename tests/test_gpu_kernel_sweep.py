@@ -19,6 +19,14 @@ import paper_2003_05293_b200 as hs
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True)
+def _fp32_kernels():
+    """These pupils hold few pixels per spot, where precision "auto" picks the
+    fp64 passes; the sweep is about the fp32 kernel instantiations."""
+    with hs.precision("fp32"):
+        yield
+
 EU_ATOL = 1e-3        # e, u absolute (north star)
 INTEN_RTOL = 1e-4     # per-spot |E_n|^2 relative (north star)
 

@@ -199,8 +199,7 @@ def test_compression_golden_table(golden, pupils):
         rep = hs.quality_report(p, holo, s)
         err = max(abs(rep.efficiency - row["e"]), abs(rep.uniformity - row["u"]))
         worst[row["iterations"]] = max(worst.get(row["iterations"], 0.0), err)
-        if row["iterations"] <= 49:
-            assert err <= EU_ATOL, (row, rep.efficiency, rep.uniformity)
+        assert err <= EU_ATOL, (row, rep.efficiency, rep.uniformity)
     print("worst |de|,|du| by iteration count:", worst)
 
 
@@ -252,11 +251,13 @@ def test_underdetermined_warning_and_errors(pupils, rng):
 
 
 def test_large_spot_count_path(pupils, rng):
-    """N > 512 uses the 32-lane x 32-spot variant; compare with the oracle."""
+    """N > 512 uses the 32-lane x 32-spot fp32 variant; compare with the oracle.
+    (5 pixels per spot: precision "auto" would run fp64, so fp32 is forced.)"""
     p = pupils["p64u0"]
     s = hs.SpotSet(x=rng.uniform(-1e-4, 1e-4, 600), y=rng.uniform(-1e-4, 1e-4, 600),
                    z=rng.uniform(-5e-5, 5e-5, 600), amplitude=np.ones(600))
-    holo, trace = hs.wgs(p, s, iterations=3, seed=1)
+    with hs.precision("fp32"):
+        holo, trace = hs.wgs(p, s, iterations=3, seed=1)
     r = oracle.solve(p, s.x, s.y, s.z, s.amplitude, "wgs", 3, seed=1)
     mags = np.array([rec.magnitudes for rec in trace.records])
     assert np.all(np.abs(mags - r["mags"]) <= 1e-4 * r["mags"])

@@ -26,9 +26,10 @@ def test_compare_at_budget_reproduces_golden_table(golden, pupils):
         assert (rec.algorithm, rec.c, rec.seed) == (row["algorithm"], row["c"], row["seed"])
         assert rec.iterations == row["iterations"] and rec.ops == row["ops"]
         assert "failed" not in rec.flags
-        if row["iterations"] <= 49:   # longer compressed runs are chaotic
-            assert abs(rec.efficiency - row["e"]) <= EU_ATOL, (row, rec)
-            assert abs(rec.uniformity - row["u"]) <= EU_ATOL, (row, rec)
+        # every row, including the long compressed runs (I = 97, 193): the
+        # small windows run the fp64 passes under precision "auto"
+        assert abs(rec.efficiency - row["e"]) <= EU_ATOL, (row, rec)
+        assert abs(rec.uniformity - row["u"]) <= EU_ATOL, (row, rec)
     assert summary.rs.runs == summary.wgs.runs == 5
     assert summary.best in summary.cswgs_cells
     assert summary.best_c in cs

@@ -19,12 +19,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def test_parity_with_ffma_full_pass():
-    env = dict(os.environ, HS_UMMA="0")
+    env = dict(os.environ, HS_UMMA="0", HS_PRECISION="fp32")
     r = subprocess.run(
         [sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
-         os.path.join(HERE, "test_gpu_parity.py"),
-         "-k", "solver_matches or quality_gate or bitwise or wgs_equals or trace_weight or pipelined"],
+         os.path.join(HERE, "test_gpu_parity.py"), os.path.join(HERE, "test_gpu_spot_chunks.py"),
+         "-k", "solver_matches or quality_gate or bitwise or wgs_equals or trace_weight or pipelined"
+               " or spot_chunk"],
         env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     m = re.search(r"(\d+) passed", r.stdout)
-    assert m and int(m.group(1)) >= 12, r.stdout[-2000:]
+    assert m and int(m.group(1)) >= 21, r.stdout[-2000:]
