@@ -103,6 +103,27 @@ int hs_get_precision(hs_plan *plan, int *mode, int *last_solve);
 int hs_set_spots(hs_plan *plan, int batch, int n, const double *x,
                  const double *y, const double *z, const double *a0);
 
+/* Test hook: one device weight update (rebalance_weights, solvers.py:104-129)
+ * of n spots from weights w_in[n] and fields[2n] (a0 = 1) on the current
+ * device.  w_out / mags_out receive the new weights and the magnitudes used
+ * (floored); status: HS_OK, HS_EDEGENERATE (all fields zero) or HS_EDIVERGED
+ * (a weight left float range; outputs then undefined); degenerate: 1 when
+ * a zero magnitude was floored. */
+int hs_debug_update(int n, const double *w_in, const double *fields, double *w_out,
+                    double *mags_out, int *status, int *degenerate);
+
+/* Phasor tables of pattern 0 (SpotTables, kernels.py:61-76, 177-183):
+ * gx_re/gx_im/gy_re/gy_im are [side][n] fp64 row-major.
+ * hs_get_tables builds them on the device (the reference's operation order
+ * for the arguments, fp64 sincos) and copies them out.
+ * hs_set_tables installs caller tables for pattern 0 (batch 1, n spots) --
+ * the `tables=` argument of superpose / forward_project: the following API
+ * passes use them (rounded once to fp32 on the fp32 passes) until the spot
+ * set changes or a solve rebuilds the tables from the spots. */
+int hs_get_tables(hs_plan *plan, double *gx_re, double *gx_im, double *gy_re, double *gy_im);
+int hs_set_tables(hs_plan *plan, int n, const double *gx_re, const double *gx_im,
+                  const double *gy_re, const double *gy_im);
+
 /* Backward pass of pattern 0 over storage pixels [start, stop):
  * out[stop-start] receives wrapped phases (kernels.py:186-214).
  * amplitude/theta: [n] superposition coefficients (SpotCoefficients). */

@@ -48,7 +48,8 @@ EXPORTS = (
     "hs_host_free", "hs_probe", "hs_solve_host_async", "hs_shard_begin", "hs_shard_pass",
     "hs_shard_update", "hs_padded_spots", "hs_shard_groups", "hs_raster", "hs_get_raster",
     "hs_shard_p2p_setup", "hs_shard_p2p_open", "hs_shard_p2p_pass", "hs_shard_p2p_close",
-    "hs_set_precision", "hs_get_precision",
+    "hs_set_precision", "hs_get_precision", "hs_get_tables", "hs_set_tables",
+    "hs_debug_update",
 )
 
 IPC_HANDLE_BYTES = 64  # HS_IPC_HANDLE_BYTES
@@ -109,6 +110,9 @@ def load():
             "hs_shard_p2p_close": (I, [P]),
             "hs_set_precision": (I, [P, I]),
             "hs_get_precision": (I, [P, ctypes.POINTER(I), ctypes.POINTER(I)]),
+            "hs_get_tables": (I, [P, P, P, P, P]),
+            "hs_set_tables": (I, [P, I, P, P, P, P]),
+            "hs_debug_update": (I, [I, P, P, P, P, ctypes.POINTER(I), ctypes.POINTER(I)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -234,6 +238,21 @@ class Plan:
         mode, last = ctypes.c_int(), ctypes.c_int()
         check(load().hs_get_precision(self.handle, ctypes.byref(mode), ctypes.byref(last)))
         return "fp64" if last.value == PREC_FP64 else "fp32"
+
+    def get_tables(self):
+        """fp64 phasor tables of pattern 0: (gx_re, gx_im, gy_re, gy_im), [side][n]."""
+        out = [np.empty((self.side, self.n)) for _ in range(4)]
+        check(load().hs_get_tables(self.handle, *[ptr(o) for o in out]))
+        return tuple(out)
+
+    def set_tables(self, gx_re, gx_im, gy_re, gy_im) -> None:
+        """Install caller tables for pattern 0 (kept until the spots change)."""
+        arrs = [f64(a) for a in (gx_re, gx_im, gy_re, gy_im)]
+        if any(a.shape != (self.side, self.n) for a in arrs):
+            raise InvalidParameterError(
+                f"tables must be ({self.side}, {self.n}) arrays, got {[a.shape for a in arrs]}")
+        check(load().hs_set_tables(self.handle, self.n, *[ptr(a) for a in arrs]))
+        self._spots_key = None   # the next set_spots re-uploads (and rebuilds the tables)
 
     # ---- kernels --------------------------------------------------------
     def superpose(self, amplitude, theta, start: int, stop: int) -> np.ndarray:

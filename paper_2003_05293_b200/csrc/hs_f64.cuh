@@ -209,6 +209,30 @@ __global__ void __launch_bounds__(kP64Threads) hs_pass64_kernel(const Pass64Args
     }
 }
 
+// user tables (hs_set_tables / hs_get_tables): [side][n] re/im planes <-> [side][np] phasors
+static __global__ void hs_pack_tables_kernel(int side, int n, int np, const double *re, const double *im,
+                                             double2 *t64, float2 *t32)
+{
+    const int j = blockIdx.x;
+    for (int k = threadIdx.x; k < np; k += blockDim.x) {
+        const double2 v = k < n ? make_double2(re[(int64_t)j * n + k], im[(int64_t)j * n + k])
+                                : make_double2(0.0, 0.0);
+        t64[(int64_t)j * np + k] = v;
+        t32[(int64_t)j * np + k] = make_float2((float)v.x, (float)v.y);
+    }
+}
+
+static __global__ void hs_unpack_tables_kernel(int side, int n, int np, const double2 *t64, double *re,
+                                               double *im)
+{
+    const int j = blockIdx.x;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const double2 v = t64[(int64_t)j * np + k];
+        re[(int64_t)j * n + k] = v.x;
+        im[(int64_t)j * n + k] = v.y;
+    }
+}
+
 typedef void (*Pass64Fn)(Pass64Args);
 
 inline Pass64Fn hs_select_pass64(int mode)

@@ -222,6 +222,7 @@ struct hs_plan {
     double2 *d_coef64 = nullptr;          // [B][np]
     double2 *d_part64 = nullptr;          // [B][part_stride]
     bool tables64_valid = false;
+    bool user_tables = false;             // pattern 0's tables came from hs_set_tables
 
     int last_alg = -1, last_iters = 0, last_flags = 0;
     // row-sharded solve state (hs_shard_*)
@@ -1352,7 +1353,117 @@ int hs_set_spots(hs_plan *p, int batch, int n, const double *x, const double *y,
     CUDA_TRY(cudaMemcpyAsync(p->d_a0, a0, bytes, cudaMemcpyHostToDevice, p->stream));
     p->tables_valid = false;
     p->tables64_valid = false;
+    p->user_tables = false;
     return HS_OK;
+}
+
+// Test hook: one weight / theta update (hs_update, the device restatement of
+// rebalance_weights, solvers.py:104-129) on caller fields -- the reference's
+// floor-and-flag, all-zero and divergence cases run through the device code.
+static __global__ void __launch_bounds__(kThreads) hs_update_probe_kernel(UpdArgs u, const double2 *E_in)
+{
+    __shared__ double dbuf[kThreads];
+    __shared__ int ibuf[kThreads];
+    extern __shared__ double2 Es[];     // [np] fields + [2 np] scratch
+    for (int k = threadIdx.x; k < u.np; k += kThreads) Es[k] = k < u.n ? E_in[k] : make_double2(0.0, 0.0);
+    __syncthreads();
+    hs_update(u, 0, Es, reinterpret_cast<double *>(Es + u.np), dbuf, ibuf);
+}
+
+int hs_debug_update(int n, const double *w_in, const double *fields, double *w_out, double *mags_out,
+                    int *status, int *degenerate)
+{
+    if (n < 1 || n > kMaxSpots) return fail(HS_EINVAL, "spot count %d outside 1..%d", n, kMaxSpots);
+    const int np = 32 * ((n + 31) / 32);
+    double *buf = nullptr;
+    int32_t *ibuf = nullptr;
+    // w [np] | a0 [n] | trace_w [n] | trace_m [n] | E [2 np] | coef64 [2 np]
+    int rc;
+    if ((rc = dalloc(&buf, (size_t)np + 3 * n + 4 * np)) || (rc = dalloc(&ibuf, 3))) {
+        if (buf) cudaFree(buf);
+        return rc;
+    }
+    double *w = buf, *a0 = w + np, *tw = a0 + n, *tm = tw + n, *E = tm + n, *coef = E + 2 * np;
+    std::vector<double> ones(n, 1.0);
+    CUDA_TRY(cudaMemset(buf, 0, sizeof(double) * ((size_t)np + 3 * n + 4 * np)));
+    CUDA_TRY(cudaMemset(ibuf, 0, sizeof(int32_t) * 3));
+    CUDA_TRY(cudaMemcpy(w, w_in, sizeof(double) * n, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(a0, ones.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(E, fields, sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
+    UpdArgs u;
+    memset(&u, 0, sizeof u);
+    u.act = ACT_STEP;
+    u.n = n;
+    u.np = np;
+    u.a0 = a0;
+    u.w = w;
+    u.coef64 = reinterpret_cast<double2 *>(coef);
+    u.trace_w = tw;
+    u.trace_m = tm;
+    u.iters = 1;
+    u.status = ibuf;
+    u.degen = ibuf + 1;
+    u.qstatus = ibuf + 2;
+    hs_update_probe_kernel<<<1, kThreads, 32 * np>>>(u, reinterpret_cast<const double2 *>(E));
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    int32_t st[3];
+    CUDA_TRY(cudaMemcpy(st, ibuf, sizeof st, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(w_out, tw, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(mags_out, tm, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    cudaFree(buf);
+    cudaFree(ibuf);
+    *status = st[0];
+    *degenerate = st[1] != 0;
+    return HS_OK;
+}
+
+int hs_set_tables(hs_plan *p, int n, const double *gx_re, const double *gx_im, const double *gy_re,
+                  const double *gy_im)
+{
+    if (p->batch != 1) return fail(HS_EINVAL, "hs_set_tables needs a single-pattern spot set");
+    if (n != p->n) return fail(HS_EINVAL, "table spot count %d != spot count %d", n, p->n);
+    int rc;
+    if ((rc = check_device(p)) || (rc = ensure64(p))) return rc;
+    const size_t cnt = (size_t)p->side * n;
+    double *tmp = nullptr;
+    if ((rc = dalloc(&tmp, 4 * cnt))) return rc;
+    const double *src[4] = {gx_re, gx_im, gy_re, gy_im};
+    for (int q = 0; q < 4; ++q)
+        CUDA_TRY(cudaMemcpyAsync(tmp + q * cnt, src[q], sizeof(double) * cnt, cudaMemcpyHostToDevice, p->stream));
+    hs_pack_tables_kernel<<<p->side, 128, 0, p->stream>>>(p->side, n, p->cfg.np, tmp, tmp + cnt, p->d_gx64, p->d_gx);
+    hs_pack_tables_kernel<<<p->side, 128, 0, p->stream>>>(p->side, n, p->cfg.np, tmp + 2 * cnt, tmp + 3 * cnt,
+                                                          p->d_gy64, p->d_gy);
+    CUDA_TRY(cudaGetLastError());
+    rc = sync_and_check(p);
+    cudaFree(tmp);
+    if (rc) return rc;
+    p->tables_valid = p->tables64_valid = true;
+    p->user_tables = true;
+    return HS_OK;
+}
+
+int hs_get_tables(hs_plan *p, double *gx_re, double *gx_im, double *gy_re, double *gy_im)
+{
+    if (p->batch < 1) return fail(HS_EINVAL, "no spots set");
+    int rc;
+    if ((rc = check_device(p))) return rc;
+    p->use64 = true;
+    rc = ensure_tables(p);
+    p->use64 = false;
+    if (rc) return rc;
+    const size_t cnt = (size_t)p->side * p->n;
+    double *tmp = nullptr;
+    if ((rc = dalloc(&tmp, 4 * cnt))) return rc;
+    hs_unpack_tables_kernel<<<p->side, 128, 0, p->stream>>>(p->side, p->n, p->cfg.np, p->d_gx64, tmp, tmp + cnt);
+    hs_unpack_tables_kernel<<<p->side, 128, 0, p->stream>>>(p->side, p->n, p->cfg.np, p->d_gy64, tmp + 2 * cnt,
+                                                            tmp + 3 * cnt);
+    double *dst[4] = {gx_re, gx_im, gy_re, gy_im};
+    for (int q = 0; q < 4; ++q)
+        CUDA_TRY(cudaMemcpyAsync(dst[q], tmp + q * cnt, sizeof(double) * cnt, cudaMemcpyDeviceToHost, p->stream));
+    rc = sync_and_check(p);
+    cudaFree(tmp);
+    return rc;
 }
 
 static int check_range(hs_plan *p, int64_t start, int64_t stop)
@@ -1568,6 +1679,10 @@ static int solve_into(hs_plan *p, int alg, int iters, int64_t subset, const doub
     }
     CUDA_TRY(cudaGraphLaunch(it->second, p->stream));
     p->out_slot = slot;
+    if (p->user_tables) {  // the solve rebuilt the tables from the spots
+        p->tables_valid = p->tables64_valid = false;
+        p->user_tables = false;
+    }
     if (p->use64) p->tables64_valid = true;
     else p->tables_valid = true;
     p->last_precision = p->use64 ? HS_PREC_FP64 : HS_PREC_FP32;

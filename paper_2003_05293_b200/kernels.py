@@ -43,18 +43,78 @@ class SpotCoefficients:
         return int(self.amplitude.shape[0])
 
 
-@dataclass(frozen=True)
 class SpotTables:
-    """Handle for one (pupil, spots) pairing (kernels.py:61-76).
+    """Per-spot column/row phasor tables (kernels.py:61-76).
 
-    The phasor tables themselves live on the device, rebuilt by the table
-    kernel whenever the spot batch changes; this handle only pins the pair
-    so callers can pass ``tables=`` exactly as with the reference.
+    ``gx[j, n] = exp(i (c1 x_n axis[j] + c2 z_n axis[j]^2))``, ``gy`` likewise
+    with ``y_n``; fp64 [side, n] arrays ``gx_re, gx_im, gy_re, gy_im`` and
+    ``count``, as the reference.  :func:`spot_tables` builds them on the device
+    (the solver's own table kernel, fp64) and copies them to the host on first
+    access; constructing one from arrays (``SpotTables(gx_re, gx_im, gy_re,
+    gy_im, count)``) gives caller tables, which ``tables=`` then uploads and
+    the passes use instead of tables derived from the spot positions.
     """
 
-    pupil: Pupil
-    spots: SpotSet
-    count: int
+    __slots__ = ("count", "_arrays", "_source")
+
+    def __init__(self, gx_re=None, gx_im=None, gy_re=None, gy_im=None, count=None, *,
+                 _source=None):
+        object.__setattr__(self, "_source", _source)
+        if _source is not None:
+            object.__setattr__(self, "_arrays", None)
+            object.__setattr__(self, "count", int(_source[1].count))
+            return
+        arrs = []
+        for a in (gx_re, gx_im, gy_re, gy_im):
+            v = np.array(a, dtype=np.float64)
+            v.setflags(write=False)
+            arrs.append(v)
+        if arrs[0].ndim != 2 or any(v.shape != arrs[0].shape for v in arrs):
+            raise InvalidParameterError("tables must be four equal-shape 2-D arrays")
+        object.__setattr__(self, "_arrays", tuple(arrs))
+        object.__setattr__(self, "count", int(arrs[0].shape[1] if count is None else count))
+
+    def __setattr__(self, name, value):
+        raise AttributeError("SpotTables is immutable")
+
+    def _get(self):
+        if self._arrays is None:
+            pupil, spots = self._source
+            plan = _lib.plan_for(pupil)
+            plan.set_spots(spots)
+            arrs = plan.get_tables()
+            for v in arrs:
+                v.setflags(write=False)
+            object.__setattr__(self, "_arrays", arrs)
+        return self._arrays
+
+    @property
+    def gx_re(self) -> np.ndarray:
+        return self._get()[0]
+
+    @property
+    def gx_im(self) -> np.ndarray:
+        return self._get()[1]
+
+    @property
+    def gy_re(self) -> np.ndarray:
+        return self._get()[2]
+
+    @property
+    def gy_im(self) -> np.ndarray:
+        return self._get()[3]
+
+
+def _use_tables(plan, pupil: Pupil, spots: SpotSet, tables) -> None:
+    """Bind the spot set (and caller tables, if any) to the device plan."""
+    plan.set_spots(spots)
+    if tables is None:
+        return
+    if tables._source is not None and tables._source[0] is pupil and tables._source[1] is spots:
+        return   # device-built for exactly these spots: the plan rebuilds the same tables
+    if tables.count != spots.count:
+        raise InvalidParameterError(f"tables carry {tables.count} spots, spot set {spots.count}")
+    plan.set_tables(tables.gx_re, tables.gx_im, tables.gy_re, tables.gy_im)
 
 
 def effective_workers(workers: int) -> int:
@@ -74,9 +134,8 @@ def _check_range(pixel_range, m: int) -> tuple[int, int]:
 
 
 def spot_tables(pupil: Pupil, spots: SpotSet) -> SpotTables:
-    plan = _lib.plan_for(pupil)
-    plan.set_spots(spots)
-    return SpotTables(pupil, spots, spots.count)
+    """Phasor tables of (pupil, spots) (kernels.py:177-183), built on the device."""
+    return SpotTables(_source=(pupil, spots))
 
 
 def superpose(pupil: Pupil, spots: SpotSet, coeffs: SpotCoefficients, pixel_range=None,
@@ -90,7 +149,7 @@ def superpose(pupil: Pupil, spots: SpotSet, coeffs: SpotCoefficients, pixel_rang
     if stop == start:
         return np.empty(0, dtype=np.float64)
     plan = _lib.plan_for(pupil)
-    plan.set_spots(spots)
+    _use_tables(plan, pupil, spots, tables)
     return plan.superpose(coeffs.amplitude, coeffs.theta, start, stop)
 
 
@@ -108,7 +167,7 @@ def forward_project(pupil: Pupil, hologram: Hologram, spots: SpotSet, pixel_rang
     if stop == start:
         return np.zeros(spots.count, dtype=np.complex128)
     plan = _lib.plan_for(pupil)
-    plan.set_spots(spots)
+    _use_tables(plan, pupil, spots, tables)
     return plan.forward(hologram.phase, start, stop)
 
 

@@ -158,10 +158,20 @@ def _run_batch(algorithm: str, pupil: Pupil, spot_sets, iterations: int, subset:
     else:
         theta0 = np.ascontiguousarray(theta0, dtype=np.float64).reshape(len(spot_sets), n)
     iters = 0 if algorithm == "rs" else iterations
-    plan.solve(_ALG_CODE[algorithm], iters, subset, theta0, want_fields=True, raster=raster)
+    # the fused e/u projection needs illumination (metrics.py:37-38); without
+    # it RS still succeeds and WGS / CS-WGS fail on the all-zero fields with
+    # DegenerateFieldError, as in the reference (solvers.py:117-119)
+    lit = pupil.sum_amplitude > 0.0
+    plan.solve(_ALG_CODE[algorithm], iters, subset, theta0, want_fields=lit, raster=raster)
     status, deg = plan.status()
     w, mg = plan.trace(iters)
-    e, u, inten, rel, fields = plan.quality_batch()
+    if lit:
+        e, u, inten, rel, fields = plan.quality_batch()
+    else:
+        b = plan.batch
+        e, u = np.full(b, np.nan), np.full(b, np.nan)
+        inten, rel = np.full((b, n), np.nan), np.full((b, n), np.nan)
+        fields = np.full((b, n), np.nan, dtype=np.complex128)
     phases = plan.phases() if fetch_phase else np.empty((plan.batch, 0))
     return BatchResult(phases, w, mg, status, deg, e, u, inten, rel, fields)
 
@@ -181,8 +191,11 @@ def _assemble(algorithm: str, pupil: Pupil, spots: SpotSet, res: BatchResult, b:
     m, n = pupil.active_count, spots.count
     holo = Hologram(res.phases[b], pupil)
     from .metrics import QualityReport
-    fused = QualityReport(efficiency=float(res.efficiency[b]), uniformity=float(res.uniformity[b]),
-                          intensities=res.intensities[b].copy(), target_relative=res.relative[b].copy())
+    fused = None
+    if np.isfinite(res.efficiency[b]):   # no fused estimate for an unlit pupil
+        fused = QualityReport(efficiency=float(res.efficiency[b]), uniformity=float(res.uniformity[b]),
+                              intensities=res.intensities[b].copy(),
+                              target_relative=res.relative[b].copy())
     if algorithm == "rs":
         trace = SolverTrace("rs", (), m * n, time.perf_counter() - t0, False, holo, fused)
         return holo, trace
@@ -287,7 +300,7 @@ def wgs_step(pupil: Pupil, spots: SpotSet, state: WgsState, pixel_range=None,
     runs on the host like the reference's.  Solver runs never call this (they
     keep the whole loop on the device)."""
     fields = forward_project(pupil, state.hologram, spots, pixel_range, chunk=chunk,
-                             workers=workers)
+                             workers=workers, tables=tables)
     mags = np.hypot(fields.real, fields.imag)
     weights, mags, degenerate = rebalance_weights(state.weights, mags)
     amplitudes = weights * spots.amplitude
@@ -295,7 +308,7 @@ def wgs_step(pupil: Pupil, spots: SpotSet, state: WgsState, pixel_range=None,
     if write_range is None:
         write_range = pixel_range
     frag = superpose(pupil, spots, SpotCoefficients(amplitudes, thetas), write_range,
-                     workers=workers)
+                     workers=workers, tables=tables)
     start, stop = (0, pupil.active_count) if write_range is None else write_range
     phase = np.array(state.hologram.phase)
     phase[start:stop] = frag

@@ -58,6 +58,16 @@ def test_spot_count_variants(n):
     _check(p, s, "cswgs", 6, 0.25, seed=n)
 
 
+@pytest.mark.parametrize("side,n", [(37, 40), (50, 48), (101, 64), (101, 120), (75, 33)])
+def test_odd_sides(side, n):
+    """Sides with side % 4 != 0: the scalar column paths and the clamped /
+    zero-padded tail columns of the tcgen05 and slab kernels."""
+    p = hs.build_pupil(side, seed=side, waist=side * 4e-6)
+    s = hs.random_foci(n, 700 + side, xy=5e-5, z=2e-5)
+    _check(p, s, "cswgs", 5, 0.5, seed=side)
+    _check(p, s, "wgs", 3, 1.0, seed=side)
+
+
 def test_multi_slab_window_lists():
     """np = 128 at side 256: the window lists span two column slabs."""
     p = hs.build_pupil(256, seed=1, waist=2e-3)

@@ -39,6 +39,7 @@ def masked_phase_check(pupil, spots, got, amps, thetas, idx=None, tab=None):
     assert np.all(d[ok] <= PHASE_TOL), float(np.max(d[ok]))
     wmean = float(np.sum(d * mag) / np.sum(mag))
     assert wmean <= 1e-5, wmean
+    assert ok.mean() >= 0.99, float(ok.mean())   # the mask drops < 1% of pixels
     return float(np.max(d[ok])), float(ok.mean())
 
 
@@ -305,3 +306,21 @@ def test_pipelined_host_api_matches_batch(pupils):
             assert e[b] == want[b][1].quality.efficiency and u[b] == want[b][1].quality.uniformity
     for ptr in keep:
         lib.hs_host_free(ptr)
+
+
+def test_unlit_pupil_semantics():
+    """sum_amplitude == 0 (a gaussian waist far below the pixel pitch on an
+    even grid): RS still returns a hologram, WGS / CS-WGS raise
+    DegenerateFieldError on the all-zero fields (solvers.py:117-119) and the
+    metrics raise ZeroIlluminationError (metrics.py:37-38), as the reference."""
+    p = hs.build_pupil(16, illumination="gaussian", waist=1e-9, seed=0)
+    assert p.sum_amplitude == 0.0
+    s = hs.SpotSet.from_points([[1e-5, 0.0, 0.0], [0.0, 2e-5, 1e-5]])
+    holo, trace = hs.rs(p, s, seed=0)
+    assert np.all(np.isfinite(holo.phase)) and trace.quality is None
+    with pytest.raises(hs.DegenerateFieldError):
+        hs.wgs(p, s, iterations=3)
+    with pytest.raises(hs.DegenerateFieldError):
+        hs.cswgs(p, s, iterations=4, compression=0.5)
+    with pytest.raises(hs.ZeroIlluminationError):
+        hs.quality_report(p, holo, s)

@@ -65,6 +65,19 @@ def test_probe_at_spot_equals_metric(pupils, rng):
     assert np.array_equal(inten, probed)
 
 
+def test_probe_on_spot_bitwise_any_count_fp64(pupils, rng):
+    """fp64 passes: the per-spot sums do not depend on the spot count, so a
+    probe batch of a different size reproduces spot_intensities bit for bit."""
+    p = pupils["p64u0"]
+    spots = random_spots(rng, 3)
+    with hs.precision("fp64"):
+        holo, _ = hs.wgs(p, spots, iterations=4, seed=1)
+        inten = hs.spot_intensities(p, holo, spots)
+        extra = np.concatenate([spots.points(), rng.uniform(-5e-5, 5e-5, (40, 3))])
+        probed = hs.probe_intensities(p, holo, extra)
+    assert np.array_equal(inten, probed[:3])
+
+
 def test_two_photon_is_square(pupils, rng):
     p = pupils["p64u0"]
     holo, _ = hs.rs(p, random_spots(rng, 2), seed=0)
