@@ -12,7 +12,9 @@ value  : holograms/s over the whole job, inputs resident in HBM, CUDA-event
          timed per step on the solver stream (L2 flushed between steps).
 e2e    : the same through the C ABI (hs_solve_host) with pinned host
          buffers: spot + theta0 upload, solve, phase[B][M] float64 +
-         e/u download inside the timed region.
+         e/u download inside the timed region (the phases cross the link as
+         4-byte codes and are widened to the identical f64 values on the
+         host threads, inside the timed region).
 --impl reference : the CPU oracle (bit-exact restatement of the reference
          numba kernels, oracle/) on all host threads, one hologram per step.
 """
@@ -70,45 +72,91 @@ def pattern_arrays(first, count):
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """SM clock + throttle-reason sampler running during the timed region:
+    NVML from a thread every 5 ms (the timed region of a default run is
+    ~0.1 s), nvidia-smi at 100 ms if NVML is unavailable."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, index):
-        self.path = tempfile.mktemp(suffix=".csv")
+        import threading
+        self.sm, self.mx, self.reasons = [], 0.0, set()
+        self.proc = None
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            # CUDA_VISIBLE_DEVICES order == NVML order is not guaranteed; map by bus id
+            import torch
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            try:   # match the CUDA device by PCI bus id (CUDA and NVML orders may differ)
+                want = str(torch.cuda.get_device_properties(index).pci_bus_id).lower()[-7:]
+                for i in range(pynvml.nvmlDeviceGetCount()):
+                    hi = pynvml.nvmlDeviceGetHandleByIndex(i)
+                    bid = pynvml.nvmlDeviceGetPciInfo(hi).busId
+                    bid = (bid.decode() if isinstance(bid, bytes) else str(bid)).lower()
+                    if bid[-7:] == want:
+                        h = hi
+                        break
+            except Exception:
+                pass
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            masks = [(nm, getattr(pynvml, attr)) for nm, attr in self.REASONS]
+            self.stop_flag = threading.Event()
+
+            def loop():
+                while not self.stop_flag.is_set():
+                    self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for nm, mask in masks:
+                        if r & mask:
+                            self.reasons.add(nm)
+                    self.stop_flag.wait(0.005)
+
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            self.kind = "nvml"
+        except Exception:
+            self.kind = "smi"
+            self.path = tempfile.mktemp(suffix=".csv")
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(index),
+                     "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                     "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            except OSError:
+                self.proc = None
 
     def stop(self):
-        if self.proc is None:
+        if self.kind == "nvml":
+            self.stop_flag.set()
+            self.thread.join()
+        elif self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            names = [nm for nm, _ in self.REASONS]
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    self.sm.append(float(parts[0]))
+                    self.mx = max(self.mx, float(parts[1]))
+                except ValueError:
+                    continue
+                for nm, flag in zip(names, parts[3:7]):
+                    if flag.lower() == "active":
+                        self.reasons.add(nm)
+            os.unlink(self.path)
+        if not self.sm:
             return None
-        self.proc.terminate()
-        self.proc.wait()
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for nm, flag in zip(names, parts[3:7]):
-                if flag.lower() == "active":
-                    reasons.add(nm)
-        os.unlink(self.path)
-        if not sm:
-            return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "sampler": self.kind}
 
 
 def host_threads():
@@ -293,7 +341,6 @@ def run_ours(args):
     lib = _lib.load()
     n_in = B * NSPOTS
     h2d = 5 * n_in * 8
-    d2h = B * m * 8 + 2 * B * 8
     bufs = {}
     for name, count in (("x", n_in), ("y", n_in), ("z", n_in), ("a", n_in), ("th", n_in),
                         ("ph", B * m), ("e", B), ("u", B)):
@@ -325,6 +372,13 @@ def run_ours(args):
         e2e_call()
     e2e_plan.sync()
     e2e_s = time.perf_counter() - t0
+    # fp32 solves ship part of the batch as f64 (widened on the device) and
+    # the rest as 4-byte codes (widened on the host threads); fp64 ones f64
+    nb64 = ctypes.c_int(B)
+    if e2e_plan.last_precision() == "fp32":
+        _lib.check(lib.hs_host_copy_split(e2e_plan.handle, B, ctypes.byref(nb64)))
+    d2h = m * (8 * nb64.value + 4 * (B - nb64.value)) + 2 * B * 8
+    e2e_phase_ok = bool(np.array_equal(bufs["ph"][1].reshape(B, m)[:2], e2e_plan.phases(0, 2)))
     if dist is not None:
         t = torch.tensor([e2e_s], device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -338,7 +392,7 @@ def run_ours(args):
     # 22 launches, ~57% of the step) and of the full-range pass, each timed
     # live with CUDA events on the plan stream (hs_time_kernel)
     ms_full, pairs_full = plan.time_kernel(0, reps=10)
-    ms_final, _ = plan.time_kernel(2, reps=10)  # last iteration's pass: + f64 phase scatter
+    ms_final, _ = plan.time_kernel(3, reps=10)  # last iteration's pass: + phase-code scatter
     ms_win, pairs_win = plan.time_kernel(1, subset, reps=50)
     peak = _lib.fma_peak_tflops(local)
     flops_win = 2 * FLOP_PER_PAIR_PASS * pairs_win     # backward + forward per pair
@@ -371,8 +425,13 @@ def run_ours(args):
         "data": "synthetic", "config": workload_config(B, world),
         "e2e": {"value": e2e_value, "unit": "holograms/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps, "matches_device_e": e2e_ok,
-                "path": "hs_solve_host_async (C ABI, pinned host buffers, phase f64 storage "
-                        "order; D2H of step k overlaps the solve of step k+1)"},
+                "phase_matches_hs_get_phase": e2e_phase_ok,
+                "f64_patterns_per_step": nb64.value,
+                "path": "hs_solve_host_async (C ABI, pinned host buffers; f64 storage-order "
+                        "phases: f64_patterns_per_step of the batch widened on the device and "
+                        "copied as f64, the rest copied as 4-byte codes and widened to the "
+                        "identical f64 on the host threads; copy + widening of step k overlap "
+                        "the solve of step k+1)"},
         "roofline": {"bound": "fma", "achieved": achieved_win, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved_win / peak,
                      "traffic": traffic.get("window_pass_dram_bytes_per_launch"),

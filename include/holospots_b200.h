@@ -58,6 +58,9 @@ extern "C" {
 /* hs_solve flags */
 #define HS_WANT_FIELDS 1   /* fuse the full-range e/u projection into the last pass */
 #define HS_WANT_RASTER 2   /* also write the SLM gray raster (default linear LUT) */
+#define HS_WANT_PHASE32 4  /* fp32 solves: the last pass stores 4-byte phase codes; hs_get_phase
+                              widens them on the host to the identical f64 phases (half the
+                              device->host bytes; hs_solve_host always does this) */
 
 /* Pixel-pass arithmetic (hs_set_precision).  The reference computes in fp64
  * throughout (holospots/kernels.py:78-144).  FP32: fp32 pixel products with
@@ -186,7 +189,12 @@ int hs_get_quality(hs_plan *plan, double *e, double *u, double *intensities,
 /* End-to-end call used by bench.py's e2e leg: uploads spots + theta0 from
  * host memory, solves, and copies phases [batch][m], e[batch], u[batch]
  * back to host memory.  Equivalent to hs_set_spots + hs_solve +
- * hs_get_phase + hs_get_quality. */
+ * hs_get_phase + hs_get_quality.  fp32 solves split the phase download:
+ * the first hs_host_copy_split patterns are widened to f64 on the device and
+ * copied as f64, the rest cross the link as 4-byte codes and are widened on
+ * the host threads (HS_E2E_F64_FRAC, default 0.375; HS_E2E_CODES=0 ships all
+ * as f64) -- identical f64 bits either way. */
+int hs_host_copy_split(hs_plan *plan, int batch, int *f64_patterns);
 int hs_solve_host(hs_plan *plan, int algorithm, int iterations, int64_t subset,
                   int batch, int n, const double *x, const double *y,
                   const double *z, const double *a0, const double *theta0,
@@ -247,7 +255,8 @@ int hs_padded_spots(hs_plan *plan);
  * `reps` back-to-back launches on the plan stream) of the kernel `which`
  * (0 = full-range fused pass, 1 = compressed-window fused pass,
  * 2 = full-range fused pass of the final iteration, with the f64 phase
- * written in storage order) with the current spot batch. */
+ * written in storage order, 3 = the same storing 4-byte phase codes, as
+ * solves do) with the current spot batch. */
 void *hs_plan_stream(hs_plan *plan);
 int hs_last_launch_count(hs_plan *plan, int64_t *launches);
 int hs_time_kernel(hs_plan *plan, int which, int64_t subset, int reps,

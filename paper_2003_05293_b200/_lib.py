@@ -17,14 +17,15 @@ from .errors import (DegenerateFieldError, DeviceError, GeometryMismatchError,
                      InvalidParameterError, UndefinedUniformityError,
                      ZeroIlluminationError)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
-                        "libholospots_b200.so")
+LIB_PATH = os.environ.get("HS_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libholospots_b200.so")
 
 HS_OK, HS_EINVAL, HS_EGEOMETRY, HS_EDEGENERATE, HS_EDIVERGED, HS_ECUDA, \
     HS_EZEROILLUM, HS_EUNDEFINED = range(8)
 ALG_RS, ALG_WGS, ALG_CSWGS = 0, 1, 2
 WANT_FIELDS = 1
 WANT_RASTER = 2
+WANT_PHASE32 = 4   # fp32 solves ship 4-byte phase codes, widened on the host (same f64 bits)
 PREC_AUTO, PREC_FP32, PREC_FP64 = 0, 1, 2
 PRECISIONS = {"auto": PREC_AUTO, "fp32": PREC_FP32, "fp64": PREC_FP64}
 
@@ -49,7 +50,7 @@ EXPORTS = (
     "hs_shard_update", "hs_padded_spots", "hs_shard_groups", "hs_raster", "hs_get_raster",
     "hs_shard_p2p_setup", "hs_shard_p2p_open", "hs_shard_p2p_pass", "hs_shard_p2p_close",
     "hs_set_precision", "hs_get_precision", "hs_get_tables", "hs_set_tables",
-    "hs_debug_update",
+    "hs_debug_update", "hs_host_copy_split",
 )
 
 IPC_HANDLE_BYTES = 64  # HS_IPC_HANDLE_BYTES
@@ -113,8 +114,11 @@ def load():
             "hs_get_tables": (I, [P, P, P, P, P]),
             "hs_set_tables": (I, [P, I, P, P, P, P]),
             "hs_debug_update": (I, [I, P, P, P, P, ctypes.POINTER(I), ctypes.POINTER(I)]),
+            "hs_host_copy_split": (I, [P, I, ctypes.POINTER(I)]),
         }
         for name, (res, args) in sig.items():
+            if os.environ.get("HS_LIB_PATH") and not hasattr(lib, name):
+                continue  # an older build under A/B test (tools/ab_time.py)
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
@@ -229,7 +233,7 @@ class Plan:
         self._spots_key = None
 
     def _sync_precision(self) -> None:
-        if self._prec != _precision:
+        if self._prec != _precision and hasattr(load(), "hs_set_precision"):
             check(load().hs_set_precision(self.handle, PRECISIONS[_precision]))
             self._prec = _precision
 
@@ -286,7 +290,7 @@ class Plan:
         self._sync_precision()
         th = f64(theta0)
         fn = load().hs_solve if sync else load().hs_solve_async
-        flags = (WANT_FIELDS if want_fields else 0) | (WANT_RASTER if raster else 0)
+        flags = (WANT_FIELDS if want_fields else 0) | (WANT_RASTER if raster else 0) | WANT_PHASE32
         check(fn(self.handle, algorithm, iterations, subset, ptr(th), flags))
 
     def rasters(self, first: int = 0, count: int | None = None) -> np.ndarray:

@@ -93,6 +93,7 @@ struct PassArgs {
     const float2 *coef;       // [B][np]
     const double *phase_in;   // [B][phase_stride] (PM_FWD without PM_BWD)
     double *phase_out;        // [B][phase_stride] (PM_WRITE)
+    float *phase_out32;       // the same as 4-byte phase codes (PM_WRITE; replaces phase_out)
     unsigned char *raster;    // [B][side][side] SLM gray raster (PM_WRITE, nullable)
     int32_t side;
     int64_t phase_stride;
@@ -174,6 +175,36 @@ __device__ __forceinline__ double hs_phase_f64(float x, float y)
     if (p == 3.14159274101257324f) return 3.14159274101257324 - kTwoPi;
     if (p == -3.14159274101257324f) return -3.14159274101257324 + kTwoPi;
     return (double)p;
+}
+
+// The 4-byte phase code the f64 phase is a fixed function of: the fp32 atan2
+// (0 for S = 0).  hs_widen_phase (host, hs_plan.cu) maps it back to exactly
+// hs_phase_f64's value, so solves can ship half the bytes to the host.
+__device__ __forceinline__ float hs_phase_code(float x, float y)
+{
+    return (x == 0.f && y == 0.f) ? 0.f : hs_atan2(y, x);
+}
+
+// hs_phase_f64's value from its code (the host twin is hs_widen_phases).
+__host__ __device__ __forceinline__ double hs_widen_code(float p)
+{
+    if (p == 3.14159274101257324f) return 3.14159274101257324 - kTwoPi;
+    if (p == -3.14159274101257324f) return -3.14159274101257324 + kTwoPi;
+    return (double)p;
+}
+
+static __global__ void hs_widen_codes_kernel(const float *__restrict__ src, double *__restrict__ dst, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = hs_widen_code(src[i]);
+}
+
+// Store one pixel's phase: the f64 value, or its 4-byte code when the pass
+// writes codes (phase_out32 != nullptr).
+__device__ __forceinline__ void hs_store_phase(double *out, float *out32, int64_t idx, float x, float y)
+{
+    if (out32) out32[idx] = hs_phase_code(x, y);
+    else out[idx] = hs_phase_f64(x, y);
 }
 
 // Linear phase -> gray lookup of the default PhaseLut (fileio.py:159-213):
@@ -604,11 +635,10 @@ hs_pass_kernel(const PassArgs a)
             if (WRITE && valid && g == 0) {
                 const int64_t di = a.dst ? (int64_t)a.dst[i] : i + a.idx_base;
                 if (di >= 0) {
-                    const double ph = hs_phase_f64(sr, si);
-                    a.phase_out[(int64_t)pat * a.phase_stride + di] = ph;
+                    hs_store_phase(a.phase_out, a.phase_out32, (int64_t)pat * a.phase_stride + di, sr, si);
                     if (a.raster)
                         a.raster[(int64_t)pat * a.side * a.side + (int64_t)(rc >> 16) * a.side + (rc & 0xffff)] =
-                            hs_gray_linear(ph);
+                            hs_gray_linear(hs_phase_f64(sr, si));
                 }
             }
         } else {

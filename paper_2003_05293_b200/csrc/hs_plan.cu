@@ -30,6 +30,8 @@
 #include "hs_umma.cuh"
 #include "hs_f64.cuh"
 
+extern "C" void hs_widen_phases(const float *src, double *dst, int64_t n);  // hs_host.cu
+
 using namespace hs;
 
 namespace {
@@ -56,6 +58,7 @@ int fail(int code, const char *fmt, ...)
 
 constexpr int kColBlock = 64;  // dense layout: columns per CTA chunk
 constexpr int kSplitBatch = 16;  // batches >= this record two graph branches (record_solve)
+constexpr int kWidenChunks = 4;     // pieces of a phase-code download widened as they land
 constexpr int kMaxSpots32 = 1024;   // largest n of the fp32 pixel kernels (G = 32 lanes x NL = 32)
 constexpr int kMaxSpots = 4096;     // largest n overall (fp64 passes: the fold keeps 32 B per spot in smem)
 // precision "auto": fp64 passes when the smallest pixel set a solve projects
@@ -207,9 +210,23 @@ struct hs_plan {
     double *d_fields = nullptr, *d_e = nullptr, *d_u = nullptr, *d_inten = nullptr, *d_rel = nullptr;
     double *d_phase = nullptr;   // [cap_batch][m] API scratch = d_out[0]
     double *d_out[2] = {nullptr, nullptr};  // solver phase outputs (double-buffered)
+    // 4-byte phase codes (HS_WANT_PHASE32): device outputs, pinned host
+    // staging, which slot holds codes, and the slot being recorded
+    float *d_out32[2] = {nullptr, nullptr};
+    float *h_stage32[2] = {nullptr, nullptr};
+    bool slot32[2] = {false, false};
+    float *rec_out32 = nullptr;
+    struct WidenJob {
+        const float *src;
+        double *dst;
+        int64_t n;
+    } widen_job[2][4];                    // [slot][chunk]
     unsigned char *d_raster = nullptr;      // [cap_batch][side][side] SLM gray rasters
     int out_slot = 0, next_slot = 0;
     cudaStream_t copy_stream = nullptr;     // D2H of phases, overlapped with solves
+    cudaStream_t widen_stream[2] = {nullptr, nullptr};  // host widening of a slot's codes
+    cudaEvent_t landed[2][5] = {};                       // a slot's code chunks (+ f64 part) reached the host
+    double e2e_f64_frac = 0.375;          // hs_solve_host: share of patterns shipped as f64 (HS_E2E_F64_FRAC)
     cudaEvent_t solved[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
     double *d_trace_w = nullptr, *d_trace_m = nullptr;
     int64_t trace_cap = 0;
@@ -528,6 +545,12 @@ void free_batch(hs_plan *p)
     dfree(p->d_status); dfree(p->d_degen); dfree(p->d_qstatus);
     dfree(p->d_fields); dfree(p->d_e); dfree(p->d_u); dfree(p->d_inten); dfree(p->d_rel);
     dfree(p->d_out[1]);
+    for (int k = 0; k < 2; ++k) {
+        dfree(p->d_out32[k]);
+        if (p->h_stage32[k]) cudaFreeHost(p->h_stage32[k]);
+        p->h_stage32[k] = nullptr;
+        p->slot32[k] = false;
+    }
     dfree(p->d_raster);
     dfree(p->d_phase);
     p->d_out[0] = nullptr;
@@ -619,6 +642,18 @@ int ensure64(hs_plan *p)
         p->tables64_valid = false;
     }
     if (!p->d_part64 && (rc = dalloc(&p->d_part64, (size_t)p->cap_batch * p->part_stride))) return rc;
+    return HS_OK;
+}
+
+// 4-byte phase-code outputs and their pinned host staging (first use).
+int ensure_out32(hs_plan *p)
+{
+    const size_t cnt = (size_t)p->cap_batch * p->m;
+    for (int k = 0; k < 2; ++k) {
+        int rc;
+        if (!p->d_out32[k] && (rc = dalloc(&p->d_out32[k], cnt))) return rc;
+        if (!p->h_stage32[k]) CUDA_TRY(cudaMallocHost(&p->h_stage32[k], cnt * sizeof(float)));
+    }
     return HS_OK;
 }
 
@@ -781,6 +816,7 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     a.amp_img = p->d_amp_img;
     a.idx_img = p->d_idx_img;
     a.phase_out = phase_out ? phase_out + (int64_t)p->view0 * p->m : nullptr;
+    a.phase_out32 = (phase_out && p->rec_out32) ? p->rec_out32 + (int64_t)p->view0 * p->m : nullptr;
     a.phase_stride = p->m;
     a.raster = raster ? raster + (int64_t)p->view0 * p->side * p->side : nullptr;
     a.f = fold_args(p, ts.n, u, lo, hi);
@@ -789,7 +825,8 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     dim3 grid(hi - lo, p->batch);
     if (ts.umma) {
         if (p->prep_pending) CUDA_TRY(cudaStreamWaitEvent(p->stream, p->prep_ev, 0));  // operand planes ready
-        return launch_pass_kernel(p, hs_select_umma(c.np, write), grid, dim3(kUThreads), hs_umma_smem_bytes(c.np),
+        const int wmode = write ? (a.phase_out32 ? 2 : 1) : 0;
+        return launch_pass_kernel(p, hs_select_umma(c.np, wmode), grid, dim3(kUThreads), hs_umma_smem_bytes(c.np),
                                   a);
     }
     const int spt = (p->n + 7) / 8;
@@ -874,6 +911,7 @@ int launch_pass(hs_plan *p, int mode, const DevList &l, int64_t off, int64_t cou
     a.coef = p->d_coef + (int64_t)p->view0 * c.np;
     a.phase_in = phase_in ? phase_in + p->view0 * phase_stride : nullptr;
     a.phase_out = phase_out ? phase_out + p->view0 * phase_stride : nullptr;
+    a.phase_out32 = (phase_out && p->rec_out32) ? p->rec_out32 + p->view0 * phase_stride : nullptr;
     a.phase_stride = phase_stride;
     if (a.raster) a.raster += (int64_t)p->view0 * p->side * p->side;
     if (hi < 0) hi = geo.nchunks;
@@ -1124,6 +1162,8 @@ int sync_and_check(hs_plan *p)
 {
     CUDA_TRY(cudaStreamSynchronize(p->stream));
     if (p->copy_stream) CUDA_TRY(cudaStreamSynchronize(p->copy_stream));
+    for (int k = 0; k < 2; ++k)
+        if (p->widen_stream[k]) CUDA_TRY(cudaStreamSynchronize(p->widen_stream[k]));
     CUDA_TRY(cudaGetLastError());
     return HS_OK;
 }
@@ -1177,6 +1217,11 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
     CUDA_TRY(cudaSetDevice(device));
     CUDA_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&p->widen_stream[k], cudaStreamNonBlocking));
+        for (int q = 0; q <= kWidenChunks; ++q)
+            CUDA_TRY(cudaEventCreateWithFlags(&p->landed[k][q], cudaEventDisableTiming));
+    }
     CUDA_TRY(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&p->stream3, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&p->prep_ev, cudaEventDisableTiming));
@@ -1213,6 +1258,7 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
     if ((rc = dalloc(&p->d_axis, side)) || (rc = dalloc(&p->d_amp64, m))) return rc;
     CUDA_TRY(cudaMemcpy(p->d_axis, axis, sizeof(double) * side, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(p->d_amp64, amplitude, sizeof(double) * m, cudaMemcpyHostToDevice));
+    if (const char *env = getenv("HS_E2E_F64_FRAC")) p->e2e_f64_frac = std::min(1.0, std::max(0.0, atof(env)));
     if (const char *env = getenv("HS_PRECISION")) {
         if (!strcmp(env, "fp32")) p->precision_mode = HS_PREC_FP32;
         else if (!strcmp(env, "fp64")) p->precision_mode = HS_PREC_FP64;
@@ -1258,8 +1304,8 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
         if (const char *env = getenv("HS_UMMA")) p->umma_enabled = atoi(env) != 0;
         if (const char *env = getenv("HS_UMMA_MAXN")) p->umma_max_n = atoi(env);
         for (int np = 16; np <= kUNPC; np += 16)
-            for (int w = 0; w < 2; ++w)
-                CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_umma(np, w != 0),
+            for (int w = 0; w < 3; ++w)
+                CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_umma(np, w),
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)hs_umma_smem_bytes(np <= kUNPMax ? np : 1024)));
         CUDA_TRY(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -1300,6 +1346,7 @@ void hs_plan_destroy(hs_plan *p)
     hs_shard_p2p_close(p);
     cudaStreamSynchronize(p->stream);
     cudaStreamSynchronize(p->copy_stream);
+    for (int k = 0; k < 2; ++k) cudaStreamSynchronize(p->widen_stream[k]);
     free_batch(p);
     free_list(p->storage);
     for (auto &kv : p->dense) free_list(kv.second);
@@ -1312,6 +1359,10 @@ void hs_plan_destroy(hs_plan *p)
     dfree(p->d_utiles);
     cudaStreamDestroy(p->stream);
     cudaStreamDestroy(p->copy_stream);
+    for (int k = 0; k < 2; ++k) {
+        cudaStreamDestroy(p->widen_stream[k]);
+        for (int q = 0; q <= kWidenChunks; ++q) cudaEventDestroy(p->landed[k][q]);
+    }
     cudaStreamDestroy(p->stream2);
     cudaStreamDestroy(p->stream3);
     cudaEventDestroy(p->prep_ev);
@@ -1620,6 +1671,12 @@ int hs_probe(hs_plan *p, const double *phase, int64_t npts, const double *xyz, i
 
 static int solve_into(hs_plan *p, int alg, int iters, int64_t subset, const double *theta0, int flags, int slot);
 
+static void CUDART_CB widen_job_fn(void *arg)
+{
+    const auto *job = static_cast<const hs_plan::WidenJob *>(arg);
+    hs_widen_phases(job->src, job->dst, job->n);
+}
+
 int hs_solve_async(hs_plan *p, int alg, int iters, int64_t subset, const double *theta0, int flags)
 {
     return solve_into(p, alg, iters, subset, theta0, flags, 0);
@@ -1650,6 +1707,10 @@ static int solve_into(hs_plan *p, int alg, int iters, int64_t subset, const doub
         ~Reset64() { p->use64 = false; }
     } reset64{p};
     if (p->use64 && (rc = ensure64(p))) return rc;
+    // fp32 solves may store 4-byte phase codes (the fp64 passes store f64)
+    const bool codes = (flags & HS_WANT_PHASE32) && !p->use64;
+    if (!codes) flags &= ~HS_WANT_PHASE32;
+    if (codes && (rc = ensure_out32(p))) return rc;
     // host-side list building happens outside graph capture
     const DevList *l;
     if (!p->use64 && (rc = get_dense(p, p->cfg.spw, &l))) return rc;
@@ -1667,7 +1728,9 @@ static int solve_into(hs_plan *p, int alg, int iters, int64_t subset, const doub
     if (it == p->graphs.end()) {
         cudaGraph_t graph;
         CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+        p->rec_out32 = codes ? p->d_out32[slot] : nullptr;
         rc = record_solve(p, alg, iters, subset, flags, p->d_out[slot]);
+        p->rec_out32 = nullptr;
         cudaError_t ce = cudaStreamEndCapture(p->stream, &graph);
         if (rc) return rc;
         if (ce != cudaSuccess) return fail(HS_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce));
@@ -1679,6 +1742,7 @@ static int solve_into(hs_plan *p, int alg, int iters, int64_t subset, const doub
     }
     CUDA_TRY(cudaGraphLaunch(it->second, p->stream));
     p->out_slot = slot;
+    p->slot32[slot] = codes;
     if (p->user_tables) {  // the solve rebuilt the tables from the spots
         p->tables_valid = p->tables64_valid = false;
         p->user_tables = false;
@@ -1743,9 +1807,16 @@ int hs_get_phase(hs_plan *p, int first, int count, double *phase)
     if (first < 0 || count < 0 || first + count > p->batch) return fail(HS_EINVAL, "pattern range invalid");
     int rc;
     if ((rc = check_device(p))) return rc;
-    if (count)
-        CUDA_TRY(cudaMemcpyAsync(phase, p->d_out[p->out_slot] + (size_t)first * p->m, sizeof(double) * count * p->m,
-                                 cudaMemcpyDeviceToHost, p->stream));
+    if (!count) return sync_and_check(p);
+    const int slot = p->out_slot;
+    if (p->slot32[slot]) {  // 4-byte codes: widened to the identical f64 phases on the device
+        const size_t off = (size_t)first * p->m;
+        hs_widen_codes_kernel<<<4 * p->num_sms, 256, 0, p->stream>>>(p->d_out32[slot] + off, p->d_out[slot] + off,
+                                                                      (int64_t)count * p->m);
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaMemcpyAsync(phase, p->d_out[slot] + (size_t)first * p->m, sizeof(double) * count * p->m,
+                             cudaMemcpyDeviceToHost, p->stream));
     return sync_and_check(p);
 }
 
@@ -1778,16 +1849,63 @@ int hs_solve_host_async(hs_plan *p, int alg, int iters, int64_t subset, int batc
     if ((rc = hs_set_spots(p, batch, n, x, y, z, a0))) return rc;
     const int slot = p->next_slot;
     CUDA_TRY(cudaStreamWaitEvent(p->stream, p->copied[slot], 0));
-    if ((rc = solve_into(p, alg, iters, subset, theta0, HS_WANT_FIELDS, slot))) return rc;
+    static const bool no_codes = getenv("HS_E2E_CODES") && atoi(getenv("HS_E2E_CODES")) == 0;
+    if ((rc = solve_into(p, alg, iters, subset, theta0, HS_WANT_FIELDS | (no_codes ? 0 : HS_WANT_PHASE32), slot)))
+        return rc;
     if (e) CUDA_TRY(cudaMemcpyAsync(e, p->d_e, sizeof(double) * batch, cudaMemcpyDeviceToHost, p->stream));
     if (u) CUDA_TRY(cudaMemcpyAsync(u, p->d_u, sizeof(double) * batch, cudaMemcpyDeviceToHost, p->stream));
-    CUDA_TRY(cudaEventRecord(p->solved[slot], p->stream));
-    CUDA_TRY(cudaStreamWaitEvent(p->copy_stream, p->solved[slot], 0));
-    if (phase)
-        CUDA_TRY(cudaMemcpyAsync(phase, p->d_out[slot], sizeof(double) * (size_t)batch * p->m, cudaMemcpyDeviceToHost,
-                                 p->copy_stream));
-    CUDA_TRY(cudaEventRecord(p->copied[slot], p->copy_stream));
+    if (!(phase && p->slot32[slot])) {
+        CUDA_TRY(cudaEventRecord(p->solved[slot], p->stream));
+        CUDA_TRY(cudaStreamWaitEvent(p->copy_stream, p->solved[slot], 0));
+    }
+    const size_t cnt = (size_t)batch * p->m;
+    if (phase && p->slot32[slot]) {
+        // The phases leave the device two ways at once, splitting the work
+        // between the host link and the host cores (either alone is slower
+        // than the solve; tools/e2e_probe.py):
+        //  * patterns [0, nb64): widened to f64 on the device (hs_widen_codes,
+        //    bit-identical) and copied as f64 into the caller's buffer;
+        //  * patterns [nb64, batch): 4-byte codes copied to pinned staging in
+        //    kWidenChunks pieces, each widened on the host threads (a host
+        //    function on the slot's widen stream) as soon as it lands.
+        // Both overlap the next call's solve.
+        const int nb64 = (int)std::lround(p->e2e_f64_frac * batch);
+        const size_t c64 = (size_t)nb64 * p->m, c32 = cnt - c64;
+        if (nb64 > 0) {
+            hs_widen_codes_kernel<<<4 * p->num_sms, 256, 0, p->stream>>>(p->d_out32[slot], p->d_out[slot],
+                                                                          (int64_t)c64);
+            CUDA_TRY(cudaGetLastError());
+        }
+        CUDA_TRY(cudaEventRecord(p->solved[slot], p->stream));
+        CUDA_TRY(cudaStreamWaitEvent(p->copy_stream, p->solved[slot], 0));
+        for (int q = 0; q < kWidenChunks && c32 > 0; ++q) {
+            const size_t lo = c64 + c32 * q / kWidenChunks, hi = c64 + c32 * (q + 1) / kWidenChunks;
+            CUDA_TRY(cudaMemcpyAsync(p->h_stage32[slot] + lo, p->d_out32[slot] + lo, sizeof(float) * (hi - lo),
+                                     cudaMemcpyDeviceToHost, p->copy_stream));
+            CUDA_TRY(cudaEventRecord(p->landed[slot][q], p->copy_stream));
+            CUDA_TRY(cudaStreamWaitEvent(p->widen_stream[slot], p->landed[slot][q], 0));
+            p->widen_job[slot][q] = {p->h_stage32[slot] + lo, phase + lo, (int64_t)(hi - lo)};
+            CUDA_TRY(cudaLaunchHostFunc(p->widen_stream[slot], widen_job_fn, &p->widen_job[slot][q]));
+        }
+        if (c64 > 0)
+            CUDA_TRY(cudaMemcpyAsync(phase, p->d_out[slot], sizeof(double) * c64, cudaMemcpyDeviceToHost,
+                                     p->copy_stream));
+        CUDA_TRY(cudaEventRecord(p->landed[slot][kWidenChunks], p->copy_stream));
+        CUDA_TRY(cudaStreamWaitEvent(p->widen_stream[slot], p->landed[slot][kWidenChunks], 0));
+        CUDA_TRY(cudaEventRecord(p->copied[slot], p->widen_stream[slot]));
+    } else {
+        if (phase)
+            CUDA_TRY(cudaMemcpyAsync(phase, p->d_out[slot], sizeof(double) * cnt, cudaMemcpyDeviceToHost,
+                                     p->copy_stream));
+        CUDA_TRY(cudaEventRecord(p->copied[slot], p->copy_stream));
+    }
     p->next_slot = slot ^ 1;
+    return HS_OK;
+}
+
+int hs_host_copy_split(hs_plan *p, int batch, int *f64_patterns)
+{
+    *f64_patterns = (int)std::lround(p->e2e_f64_frac * batch);
     return HS_OK;
 }
 
@@ -2175,7 +2293,8 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
     int rc;
     if ((rc = check_device(p)) || (rc = ensure_tables(p))) return rc;
     const DevList *l;
-    if (which == 0 || which == 2) {
+    if (which == 3 && (rc = ensure_out32(p))) return rc;
+    if (which == 0 || which == 2 || which == 3) {
         rc = get_dense(p, p->cfg.spw, &l);
     } else {
         if (subset < 1 || subset > p->m) return fail(HS_EINVAL, "subset invalid");
@@ -2188,7 +2307,13 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
     const UpdArgs u = upd_args(p, ACT_FIELDS);
     auto once = [&]() -> int {
         if (which == 0) return launch_tile(p, false, u, nullptr);
-        if (which == 2) return launch_tile(p, true, u, p->d_out[0]);  // final pass: phase write
+        if (which == 2) return launch_tile(p, true, u, p->d_out[0]);  // final pass: f64 phase write
+        if (which == 3) {  // final pass: 4-byte phase codes (what solves store)
+            p->rec_out32 = p->d_out32[0];
+            const int r = launch_tile(p, true, u, p->d_out[0]);
+            p->rec_out32 = nullptr;
+            return r;
+        }
         return launch_pass(p, PM_BWD | PM_FWD, *l, 0, l->count, 0, nullptr, nullptr, 0, u);
     };
     if ((rc = reset_status(p)) || (rc = once())) return rc;

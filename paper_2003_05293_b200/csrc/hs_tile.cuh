@@ -45,6 +45,7 @@ struct TileArgs {
     const float *amp_img;     // [side][side], 0 outside the aperture
     const int32_t *idx_img;   // [side][side] storage index, -1 outside
     double *phase_out;        // [B][phase_stride] (WRITE)
+    float *phase_out32;       // the same as 4-byte phase codes (WRITE; replaces phase_out)
     unsigned char *raster;    // [B][side][side] SLM gray raster (WRITE, nullable)
     int64_t phase_stride;
     FoldArgs f;
@@ -191,9 +192,9 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tile_kernel(const TileArgs a)
             if (WRITE && in) {
                 const int32_t di = __ldg(a.idx_img + gidx);
                 if (di >= 0) {
-                    const double ph = hs_phase_f64(x, y);
-                    a.phase_out[(int64_t)pat * a.phase_stride + di] = ph;
-                    if (a.raster) a.raster[(int64_t)pat * a.side * a.side + gidx] = hs_gray_linear(ph);
+                    hs_store_phase(a.phase_out, a.phase_out32, (int64_t)pat * a.phase_stride + di, x, y);
+                    if (a.raster)
+                        a.raster[(int64_t)pat * a.side * a.side + gidx] = hs_gray_linear(hs_phase_f64(x, y));
                 }
             }
         }

@@ -144,9 +144,9 @@ __global__ void __launch_bounds__(kThreads, 2) hs_tilek_kernel(const TileArgs a)
             if (WRITE && in) {
                 const int32_t di = __ldg(a.idx_img + gidx);
                 if (di >= 0) {
-                    const double ph = hs_phase_f64(x, y);
-                    a.phase_out[(int64_t)pat * a.phase_stride + di] = ph;
-                    if (a.raster) a.raster[(int64_t)pat * a.side * a.side + gidx] = hs_gray_linear(ph);
+                    hs_store_phase(a.phase_out, a.phase_out32, (int64_t)pat * a.phase_stride + di, x, y);
+                    if (a.raster)
+                        a.raster[(int64_t)pat * a.side * a.side + gidx] = hs_gray_linear(hs_phase_f64(x, y));
                 }
             }
         }

@@ -5,12 +5,12 @@
 namespace hs {
 
 template <int NP>
-static UmmaFn pick(bool write)
+static UmmaFn pick(int write)
 {
-    return write ? hs_umma_kernel<NP, true> : hs_umma_kernel<NP, false>;
+    return write == 2 ? hs_umma_kernel<NP, 2> : write == 1 ? hs_umma_kernel<NP, 1> : hs_umma_kernel<NP, 0>;
 }
 
-UmmaFn hs_select_umma(int np, bool write)
+UmmaFn hs_select_umma(int np, int write)
 {
     switch (np) {
     case 16: return pick<16>(write);

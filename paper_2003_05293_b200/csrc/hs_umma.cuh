@@ -260,7 +260,7 @@ __device__ __forceinline__ void hs_cmma(Mma mma, uint32_t dr, uint32_t di, AOp a
     mma(di, aop(3), b[0], id, 1u);
 }
 
-template <int NP, bool WRITE>
+template <int NP, int WRITE>  // WRITE: 0 no phase, 1 f64 phases, 2 4-byte phase codes
 __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel(const TileArgs a)
 {
     static_assert(NP % 16 == 0 && (NP <= kUNPMax || NP == kUNPC), "forward N: np <= 112 or chunks of 128");
@@ -567,9 +567,13 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
                 if (row_in && c < a.side) {
                     const int32_t di = dix[jj];
                     if (di >= 0) {
-                        const double ph = hs_phase_f64(sr[jj], si[jj]);
-                        a.phase_out[(int64_t)pat * a.phase_stride + di] = ph;
-                        if (a.raster) a.raster[(int64_t)pat * a.side * a.side + prow + c] = hs_gray_linear(ph);
+                        if (WRITE == 2)
+                            a.phase_out32[(int64_t)pat * a.phase_stride + di] = hs_phase_code(sr[jj], si[jj]);
+                        else
+                            a.phase_out[(int64_t)pat * a.phase_stride + di] = hs_phase_f64(sr[jj], si[jj]);
+                        if (a.raster)
+                            a.raster[(int64_t)pat * a.side * a.side + prow + c] =
+                                hs_gray_linear(hs_phase_f64(sr[jj], si[jj]));
                     }
                 }
             }
@@ -703,6 +707,6 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
 }
 
 typedef void (*UmmaFn)(TileArgs);
-UmmaFn hs_select_umma(int np, bool write);
+UmmaFn hs_select_umma(int np, int write);  // write: 0 none, 1 f64 phases, 2 phase codes
 
 }  // namespace hs

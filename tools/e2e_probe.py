@@ -19,6 +19,7 @@ import torch  # noqa: E402
 
 import paper_2003_05293_b200 as hs  # noqa: E402
 from paper_2003_05293_b200 import _lib  # noqa: E402
+print("HS_E2E_F64_FRAC", os.environ.get("HS_E2E_F64_FRAC"), "HS_WIDEN_THREADS", os.environ.get("HS_WIDEN_THREADS"), "HS_E2E_CODES", os.environ.get("HS_E2E_CODES"))
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--batch", type=int, default=32)
@@ -118,3 +119,32 @@ plan.sync()
 gaps = [evs[i].elapsed_time(evs[i + 1]) for i in range(len(evs) - 1)]
 print("solve-completion gaps (ms):", " ".join(f"{g:.2f}" for g in gaps))
 print("host enqueue times (ms):", " ".join(f"{t * 1e3:.2f}" for t in host_t))
+
+# host widening of 4-byte phase codes (hs_widen_phases, csrc/hs_host.cu)
+lib.hs_widen_phases.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+lib.hs_widen_phases.restype = None
+src = lib.hs_host_alloc(B * m * 4)
+srcv = np.ctypeslib.as_array(ctypes.cast(src, ctypes.POINTER(ctypes.c_float)), shape=(B * m,))
+srcv[:] = np.random.default_rng(0).uniform(-3.14, 3.14, B * m).astype(np.float32)
+for _ in range(2):
+    lib.hs_widen_phases(src, bufs["ph"][0], B * m)
+t0 = time.perf_counter()
+for _ in range(5):
+    lib.hs_widen_phases(src, bufs["ph"][0], B * m)
+dt = (time.perf_counter() - t0) / 5
+print(f"host widening {B * m / 1e6:.1f} M codes: {dt * 1e3:.2f} ms")
+dev32 = torch.empty(B * m, dtype=torch.float32, device="cuda")
+host32 = torch.from_numpy(srcv)
+t0 = time.perf_counter()
+for _ in range(5):
+    host32.copy_(dev32, non_blocking=True)
+torch.cuda.synchronize()
+dt = (time.perf_counter() - t0) / 5
+print(f"pinned D2H {B * m * 4 / 1e6:.0f} MB: {dt * 1e3:.2f} ms")
+# widening while a D2H runs
+t0 = time.perf_counter()
+host.copy_(dev, non_blocking=True)
+lib.hs_widen_phases(src, bufs["ph"][0], B * m)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+print(f"widening with a concurrent 267 MB D2H: {(t1 - t0) * 1e3:.2f} ms (both {(time.perf_counter() - t0) * 1e3:.2f})")
