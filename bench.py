@@ -1,6 +1,10 @@
 """Benchmark: batched CS-WGS holograms/s on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+                    [--workload cfg3|cfg4]
+
+--gpus N without torchrun relaunches itself under torch.distributed.run with
+N ranks (one per GPU, NCCL); under torchrun the ranks come from the env.
 
 Workload (configs[2] with configs[4]'s batching): CS-WGS,
 1152x1152 gaussian pupil (M = 1,042,356), N = 100 random 3D foci
@@ -168,6 +172,16 @@ def host_threads():
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_oracle_rate(seconds=10.0, threads=None):
     """Oracle (bit-exact reference restatement) holograms/s on host cores."""
     import oracle
@@ -213,9 +227,13 @@ def run_reference(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(1, world),
+            "config": workload_config(args.batch, world),
+            "sample_per_step": "1 hologram of the batched workload per step (a bounded "
+                               "sample; holograms are independent, so the rate is per hologram)",
             "cpu_baseline": {"value": val, "unit": "holograms/s", "cores": threads,
-                             "kind": "port", "sample": f"{args.steps} holograms of the "
+                             "kind": "port", "cpu_model": cpu_model(),
+                             "threading": "OpenMP (libgomp), the reference's prange units",
+                             "sample": f"{args.steps} holograms of the "
                              "workload, 1 per step (C+OpenMP oracle, bit-exact vs reference)"},
             "e2e": {"value": val, "unit": "holograms/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
@@ -412,7 +430,12 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu:
         rate, done, threads = cpu_oracle_rate(args.cpu_seconds)
+        rate1, done1, _ = cpu_oracle_rate(max(2.0, args.cpu_seconds / 2), threads=1)
         cpu = {"value": rate, "unit": "holograms/s", "cores": threads, "kind": "port",
+               "cpu_model": cpu_model(), "threading": "OpenMP (libgomp), the reference's "
+               "prange units (pixels for the backward pass, 1024-pixel chunks forward)",
+               "workers_1": {"value": rate1, "unit": "holograms/s", "cores": 1,
+                             "sample": f"{done1} holograms"},
                "sample": f"{done} holograms of the workload (CS-WGS 1152^2 N=100 I=20 + e/u), "
                "C+OpenMP oracle bit-exact vs the reference numba kernels"}
     pairs_step = B * NSPOTS * (2 * 2 * m + 2 * (ITERS - 1) * subset)
@@ -464,6 +487,134 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(args):
+    """bench.py --gpus N outside torchrun: run N ranks under torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+CFG4_SPOTS, CFG4_ITERS = 1000, 30
+
+
+def cfg4_config(world):
+    return {"workload": "wgs_1152_n1000_i30_rowsharded", "side_px": SIDE, "spots": CFG4_SPOTS,
+            "iterations": CFG4_ITERS, "algorithm": "wgs",
+            "parallelism": f"row-sharded x{world} (one hologram cut at fold-group boundaries; "
+                           "group partials exchanged over peer memory each pass)" if world > 1
+            else "single GPU", "pupil": "gaussian waist 6 mm, pitch 9.2 um, lambda 800 nm, "
+            "f 20 mm, seed 0", "foci": "uniform xy +-150 um, z +-50 um, spot seed 4, solver seed 0",
+            "l2": "inputs (tables, lists) L2-resident; one solve = 31 full passes"}
+
+
+def run_cfg4(args):
+    """BASELINE configs[3]: WGS 1152^2 (square stand-in of the 1920x1152 panel),
+    N = 1000, I = 30 -- one hologram per step, row-sharded across the ranks
+    (distributed.solve_sharded's device path: peer-memory exchange of the
+    group partials, csrc/hs_xchg.cuh).  Strong scaling: the work per step is
+    fixed; value = holograms/s of the whole job."""
+    import torch
+    import paper_2003_05293_b200 as hs
+    from paper_2003_05293_b200 import _lib
+    from paper_2003_05293_b200.solvers import _theta0
+
+    rank, local, world = dist_env()
+    ndev = torch.cuda.device_count()
+    shared = world > ndev
+    local = local % ndev
+    torch.cuda.set_device(local)
+    _lib.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    coll_dev = "cpu" if shared else f"cuda:{local}"
+
+    def all_gather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    pupil = hs.build_pupil(SIDE)
+    m = pupil.active_count
+    spots = hs.random_foci(CFG4_SPOTS, 4, xy=150e-6)
+    plan = _lib.Plan(pupil, local)
+    plan.set_spots(spots)
+    th = _theta0(0, CFG4_SPOTS)[None, :]
+    stream = torch.cuda.ExternalStream(plan.stream(), device=torch.device("cuda", local))
+
+    if world > 1:
+        plan.shard_begin(_lib.ALG_WGS, CFG4_ITERS, m, th, rank, world)
+        plan.p2p_open(all_gather(plan.p2p_setup()))
+
+        def solve():
+            plan.shard_begin(_lib.ALG_WGS, CFG4_ITERS, m, th, rank, world)
+            for j in range(CFG4_ITERS + 1):
+                plan.p2p_pass(j)
+    else:
+        def solve():
+            plan.solve(_lib.ALG_WGS, CFG4_ITERS, m, th, want_fields=True, sync=False)
+
+    for _ in range(args.warmup):
+        solve()
+        plan.sync()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = Clocks(local)
+    for k in range(args.steps):
+        starts[k].record(stream)
+        solve()
+        ends[k].record(stream)
+    plan.sync()
+    clk = clocks.stop()
+    total_ms = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
+    status, _ = plan.status()
+    e, u, *_ = plan.quality_batch()
+    if dist is not None:
+        codes = all_gather(int(status[0]))
+        t = torch.tensor([total_ms], device=coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        if world > 1:
+            plan.p2p_close()
+    else:
+        codes = [int(status[0])]
+    if any(codes):
+        raise RuntimeError(f"sharded solve failed: {codes}")
+    if rank != 0:
+        return
+    flop = 2 * FLOP_PER_PAIR_PASS * CFG4_SPOTS * m * (CFG4_ITERS + 1)
+    ms = total_ms / args.steps
+    line = {"metric": "holograms/s (config 4: WGS 1152^2, N=1000, I=30, row-sharded)",
+            "value": 1e3 / ms, "unit": "holograms/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "ms_per_hologram": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic", "config": cfg4_config(world),
+            "achieved_tflops_fp32_equivalent": flop / (ms * 1e-3) / 1e12,
+            "e": float(e[0]), "u": float(u[0]),
+            "reference_e_u": [0.906461, 0.158003], "clocks": clk,
+            "gpu_launches": plan.last_launch_count() * args.steps if world == 1 else
+            (1 + 3 * (CFG4_ITERS + 1)) * args.steps,
+            "shared_gpu": shared}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -473,11 +624,16 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "cfg4":
+        run_cfg4(args)
     else:
         run_ours(args)
 

@@ -1264,6 +1264,11 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
         if (!strcmp(env, "fp32")) p->precision_mode = HS_PREC_FP32;
         else if (!strcmp(env, "fp64")) p->precision_mode = HS_PREC_FP64;
     }
+    // exchange / host-fold update kernels: fields + scratch of up to kMaxSpots32 spots
+    CUDA_TRY(cudaFuncSetAttribute((const void *)hs_gather_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double2) * 3 * kMaxSpots32)));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)hs_fold_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double2) * 2 * kMaxSpots32)));
     for (int mode : std::initializer_list<int>{PM_BWD | PM_WRITE, PM_FWD, PM_BWD | PM_FWD, PM_BWD | PM_FWD | PM_WRITE})
         CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_pass64(mode),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPass64SmemMax));
@@ -1991,6 +1996,7 @@ int hs_shard_begin(hs_plan *p, int alg, int iters, int64_t subset, const double 
     CUDA_TRY(cudaMemsetAsync(p->d_out[0], 0xff, sizeof(double) * (size_t)p->batch * p->m, p->stream));
     p->tables_valid = true;
     p->out_slot = 0;
+    p->slot32[0] = false;   // the sharded passes write f64 phases into d_out[0]
     p->last_alg = alg;
     p->last_iters = iters;
     p->last_flags = HS_WANT_FIELDS;
@@ -2133,6 +2139,7 @@ int hs_shard_p2p_pass(hs_plan *p, int j)
     a.flags_local = (unsigned long long *)x.local;
     a.xbuf_local = (const double2 *)(x.local + kFlagBytes);
     a.pub_cnt = x.d_cnt;
+    a.batch = p->batch;
     if (a.g_hi > a.g_lo) {
         hs_publish_kernel<<<dim3(a.g_hi - a.g_lo, p->batch), 128, 0, p->stream>>>(a);
         CUDA_TRY(cudaGetLastError());

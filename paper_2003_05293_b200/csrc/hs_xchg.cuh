@@ -19,8 +19,13 @@
 //      bitwise equal to the single-GPU solve.
 // Two slots suffice: a rank can publish pass j+2 only after its update of
 // pass j+1, which needs every rank's pass j+1 publish, which each rank
-// issues after its own update of pass j.  The spin is bounded (~2 s), and a
-// timeout marks the pattern failed instead of hanging the device.
+// issues after its own update of pass j.  The spin is bounded (2 s of
+// globaltimer), and a timeout marks the pattern failed instead of hanging
+// the device.  Failure propagates: a rank with a failed pattern (timeout,
+// degenerate fields) publishes its epoch with kXchgAbort set, and every peer
+// whose gather sees that bit marks its patterns failed too -- all ranks stop
+// together and raise together (distributed.solve_sharded all-gathers the
+// status before the phase exchange) instead of folding stale partials.
 #pragma once
 
 #include "hs_kernels.cuh"
@@ -40,7 +45,18 @@ struct XchgArgs {
     const double2 *xbuf_local;
     int32_t *pub_cnt;           // local arrival counter (self-resetting)
     int32_t announce_only;      // rank without groups: publish the epoch only
+    int32_t batch;              // patterns (status entries) of this rank
 };
+
+constexpr unsigned long long kXchgAbort = 1ull << 63;   // epoch flag bit: the publisher failed
+constexpr unsigned long long kXchgTimeoutNs = 2000000000ull;
+
+__device__ __forceinline__ unsigned long long hs_globaltimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ void hs_st_release_sys(unsigned long long *p, unsigned long long v)
 {
@@ -77,7 +93,10 @@ static __global__ void __launch_bounds__(128) hs_publish_kernel(const XchgArgs a
         if (atomicAdd(a.pub_cnt, 1) == total - 1) {
             *a.pub_cnt = 0;
             __threadfence_system();
-            for (int r = 0; r < a.world; ++r) hs_st_release_sys(a.peer_flags[r] + a.rank, a.epoch);
+            bool failed = false;   // any pattern of this rank failed: tell the peers
+            for (int b = 0; b < a.batch; ++b) failed |= (*(volatile int32_t *)(a.f.u.status + b) != 0);
+            const unsigned long long v = a.epoch | (failed ? kXchgAbort : 0ull);
+            for (int r = 0; r < a.world; ++r) hs_st_release_sys(a.peer_flags[r] + a.rank, v);
         }
     }
 }
@@ -91,20 +110,23 @@ static __global__ void __launch_bounds__(kThreads) hs_gather_update_kernel(const
     const int pat = blockIdx.x, np = a.f.np;
     if (threadIdx.x == 0) {
         int ok = 1;
-        const long long t0 = clock64();
-        for (int r = 0; r < a.world && ok; ++r)
-            while (hs_ld_acquire_sys(a.flags_local + r) < a.epoch) {
+        const unsigned long long t0 = hs_globaltimer();
+        for (int r = 0; r < a.world && ok; ++r) {
+            unsigned long long v;
+            while (((v = hs_ld_acquire_sys(a.flags_local + r)) & ~kXchgAbort) < a.epoch) {
                 __nanosleep(128);
-                if (clock64() - t0 > 4000000000LL) {  // ~2 s at 1.9 GHz: a peer never published
+                if (hs_globaltimer() - t0 > kXchgTimeoutNs) {  // a peer never published
                     ok = 0;
                     break;
                 }
             }
+            if (v & kXchgAbort) ok = 0;  // a peer failed this pass
+        }
         s_ok = ok;
     }
     __syncthreads();
     if (!s_ok) {
-        if (threadIdx.x == 0) a.f.u.status[pat] = 5;  // HS_ECUDA: exchange timed out
+        if (threadIdx.x == 0) a.f.u.status[pat] = 5;  // HS_ECUDA: exchange timed out or a peer failed
         return;
     }
     if (a.f.u.status[pat] != 0) return;

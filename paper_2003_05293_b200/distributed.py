@@ -143,7 +143,12 @@ def solve_sharded(pupil, spots, config, rank: int, world: int, all_gather, devic
     else:
         raise ValueError(f"unknown exchange {exchange!r}")
     status, deg = plan.status()
-    _raise_status(int(status[0]))
+    # every rank raises together: a failed rank (or a peer abort seen by the
+    # exchange) must not leave the others waiting in the phase exchange
+    codes = all_gather(int(status[0]))
+    bad = [c for c in codes if c != 0]
+    if bad:
+        _raise_status(int(status[0]) or bad[0])
     mine = plan.phases()[0]
     slabs = all_gather(mine)
     phase = np.full(m, np.nan)
