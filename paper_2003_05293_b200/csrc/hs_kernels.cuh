@@ -56,7 +56,6 @@ struct UpdArgs {
     double2 *coef64;          // [B][np] the same in fp64 (fp64 passes; coef unused)
     double *trace_w, *trace_m;  // [B][iters][n]
     int iter, iters;
-    int coef_scaled;          // the fields arrive as coef_k * E_k (hs_slab): divide by coef first
     int32_t *status, *degen, *qstatus;  // [B]
     double *fields;           // [B][n][2]
     double inv_norm;          // 1 / sum_amplitude^2
@@ -321,16 +320,6 @@ __device__ __forceinline__ void hs_update(const UpdArgs &a, int b, double2 *E, d
 {
     const int tid = hs_team_tid();
     const int n = a.n, np = a.np;
-    if (a.coef_scaled) {
-        // E_k = E'_k / coef_k in fp64 (coef: the fp32 values the pass used;
-        // each thread owns the same k below, so no barrier is needed)
-        for (int k = tid; k < n; k += kThreads) {
-            const float2 c = a.coef[(int64_t)b * np + k];
-            const double cr = c.x, ci = c.y, d = cr * cr + ci * ci;
-            const double er = E[k].x, ei = E[k].y;
-            E[k] = d > 0.0 ? make_double2((er * cr + ei * ci) / d, (ei * cr - er * ci) / d) : make_double2(0.0, 0.0);
-        }
-    }
     if (a.act == ACT_FIELDS || a.act == ACT_FINAL) {
         double esum = 0.0, hi = -INFINITY, lo = INFINITY;
         for (int k = tid; k < n; k += kThreads) {

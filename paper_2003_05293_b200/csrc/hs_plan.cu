@@ -860,7 +860,6 @@ int launch_slab(hs_plan *p, int mode, const DevList &l, int32_t nunits, const Up
     a.gy = p->d_gy + p->view0 * a.tab_stride;
     a.coef = p->d_coef + (int64_t)p->view0 * c.np;
     a.f = fold_args(p, nunits, u, lo, hi);
-    a.f.u.coef_scaled = 1;  // hs_slab accumulates coef * E
     const int64_t span = (hi - lo) / 2;  // chunks
     const bool half = span * p->batch * 4 < (int64_t)p->num_sms * 3;
     int best = 1;
@@ -2122,7 +2121,6 @@ int hs_shard_p2p_pass(hs_plan *p, int j)
     UpdArgs u = upd_args(p, last ? ACT_FINAL : ACT_STEP);
     u.iter = j;
     u.iters = std::max(sh.iters, 1);
-    u.coef_scaled = (kind == 1 && lst->sw > 0);  // slab window pass: coef * E partials
     XchgArgs a;
     memset(&a, 0, sizeof a);
     a.f = fold_args(p, nch, u, lo, hi);
@@ -2200,12 +2198,6 @@ int hs_shard_update(hs_plan *p, int j, const double *groups, int ngroups)
     UpdArgs u = upd_args(p, last ? ACT_FINAL : ACT_STEP);
     u.iter = j;
     u.iters = std::max(sh.iters, 1);
-    {
-        int kind, nch;
-        const DevList *lst;
-        if ((rc = shard_pass_desc(p, j, &kind, &lst, &nch))) return rc;
-        u.coef_scaled = (kind == 1 && lst->sw > 0);  // slab window pass: coef * E partials
-    }
     hs_fold_update_kernel<<<p->batch, kThreads, sizeof(double2) * 2 * np, p->stream>>>(fold_args(p, 0, u), ngroups);
     CUDA_TRY(cudaGetLastError());
     if (last) sh.active = false;

@@ -218,14 +218,12 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
         c0 = cs;
     };
 
-    // lane state (SPL spots): V = coef * gy[row] and T packed (re, im).  The
-    // run flush accumulates E' = sum V T = coef * E (no gy registers); the
-    // update divides E' by the pass's coef in fp64 (UpdArgs.coef_scaled).
-    float vr[SPL], vi[SPL];
+    // lane state (SPL spots): V = coef * gy[row], gy[row], T packed (re, im)
+    float vr[SPL], vi[SPL], yr_[SPL], yi_[SPL];
     f2x tt[SPL];
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
-        vr[k] = vi[k] = 0.f;
+        vr[k] = vi[k] = yr_[k] = yi_[k] = 0.f;
         tt[k] = 0ull;
     }
 
@@ -247,7 +245,7 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
 #pragma unroll
         for (int j = 0; j < NS; ++j) lds_vec(row + 8u * VEC * G * j, &x[VEC * j]);
     };
-    auto flush = [&]() {  // Es[stream] += V * T = coef * (gy[row] * T) ; T = 0
+    auto flush = [&]() {  // Es[stream] += Y * T ; T = 0
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
             f2x e[VEC];
@@ -255,13 +253,13 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
 #pragma unroll
             for (int h = 0; h < VEC; ++h) {
                 const int k = VEC * j + h;
-                f2_cmac(e[h], vr[k], vi[k], tt[k]);
+                f2_cmac(e[h], yr_[k], yi_[k], tt[k]);
                 tt[k] = 0ull;
             }
             sts_vec(es_a + 8u * VEC * G * j, e);
         }
     };
-    auto new_row = [&](int r) {  // V = coef * gy[r]
+    auto new_row = [&](int r) {  // Y = gy[r], V = coef * Y
         const float2 *yrow = Y + (int64_t)r * NP;
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
@@ -270,6 +268,8 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
                 const int k = VEC * j + h;
                 const float2 q = __ldg(yrow + VEC * G * j + h);
                 const float2 w = hs_lds2(cf_a + 8u * (VEC * G * j + h));
+                yr_[k] = q.x;
+                yi_[k] = q.y;
                 vr[k] = fmaf(w.x, q.x, -w.y * q.y);
                 vi[k] = fmaf(w.x, q.y, w.y * q.x);
             }
