@@ -55,4 +55,22 @@ __device__ __forceinline__ void f2_cmac(f2x &acc, float vr, float vi, f2x x)
     f2_fma(acc, f2_pack(-xh, xl), f2_pack(vi, vi));
 }
 
+// The same complex MAC as one asm statement: the broadcast packs and the
+// swapped, negated x live inside the statement, so the compiler cannot
+// hoist or share them across MACs as materialised register pairs (which
+// costs moves and registers); ptxas folds them into the two FFMA2.
+__device__ __forceinline__ void f2_cmac1(f2x &acc, float vr, float vi, f2x x)
+{
+    asm("{\n .reg .b64 vv, ww, xs;\n .reg .f32 xl, xh;\n"
+        " mov.b64 vv, {%1, %1};\n"
+        " fma.rn.f32x2 %0, vv, %3, %0;\n"
+        " mov.b64 {xl, xh}, %3;\n"
+        " neg.f32 xh, xh;\n"
+        " mov.b64 xs, {xh, xl};\n"
+        " mov.b64 ww, {%2, %2};\n"
+        " fma.rn.f32x2 %0, xs, ww, %0;\n}"
+        : "+l"(acc)
+        : "f"(vr), "f"(vi), "l"(x));
+}
+
 }  // namespace hs

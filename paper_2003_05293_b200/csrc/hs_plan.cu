@@ -1316,8 +1316,8 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
         CUDA_TRY(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
         if (const char *env = getenv("HS_PDL")) p->pdl_enabled = atoi(env) != 0;
         for (int ns = 1; ns <= 8; ++ns)
-            for (int h = 0; h < 2; ++h)
-                CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_slab(ns, h != 0),
+            for (int h = 0; h < 4; ++h)
+                CUDA_TRY(cudaFuncSetAttribute((const void *)hs_select_slab(ns, (h & 1) != 0, h >= 2),
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               kSlabSmemBudget));  // process-wide cap: never lower it per plan
         for (int w = 0; w < 2; ++w)

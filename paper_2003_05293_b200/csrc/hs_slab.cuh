@@ -105,6 +105,20 @@ __device__ __forceinline__ void hs_bvec(float sr, float si, float A, float &br, 
     }
 }
 
+// hs_bvec without branches: S is scaled by the power of two 2^-e that
+// brings max(|Sr|, |Si|) into [1, 2) before |S|^2 is formed.  Scaling by a
+// power of two is exact, so wherever hs_bvec takes its fast path the result
+// is bitwise the same; tiny and huge |S| need no separate path.
+__device__ __forceinline__ void hs_bvec_nb(float sr, float si, float A, float &br, float &bi)
+{
+    const float mx = fmaxf(fabsf(sr), fabsf(si));
+    const float sc = __int_as_float(0x7f000000 - (__float_as_int(mx) & 0x7f800000));  // 2^-e (2^127 for denormals)
+    const float xr = sr * sc, xi = si * sc;
+    const float inv = A * hs_rsqrt(fmaf(xr, xr, xi * xi));
+    br = mx > 0.f ? xr * inv : A;
+    bi = mx > 0.f ? -xi * inv : 0.f;
+}
+
 __device__ __forceinline__ float2 hs_lds2(uint32_t addr)
 {
     float2 v;
@@ -112,7 +126,12 @@ __device__ __forceinline__ float2 hs_lds2(uint32_t addr)
     return v;
 }
 
-template <int NS, int G, bool HALF>
+// PIPE = false: pair trips (two pixels of a run per trip, transpose-reduce
+// across the two halves of the lane group).  PIPE = true: one pixel per step,
+// software-pipelined -- the butterfly of pixel t runs while the backward of
+// pixel t+1 issues (both in one basic block, so ptxas interleaves the
+// shuffle latency with FFMA2 work); see the main loop below.
+template <int NS, int G, bool HALF, bool PIPE = false>
 __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(const SlabArgs a)
 {
     constexpr int WPC = G;              // warps of a whole chunk (32 streams)
@@ -253,7 +272,7 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
 #pragma unroll
             for (int h = 0; h < VEC; ++h) {
                 const int k = VEC * j + h;
-                f2_cmac(e[h], yr_[k], yi_[k], tt[k]);
+                f2_cmac1(e[h], yr_[k], yi_[k], tt[k]);
                 tt[k] = 0ull;
             }
             sts_vec(es_a + 8u * VEC * G * j, e);
@@ -322,8 +341,8 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
         f2x m0 = 0ull, m1 = 0ull, o0 = 0ull, o1 = 0ull;
 #pragma unroll
         for (int k = 0; k < SPL; ++k) {
-            f2_cmac((k & 1) ? m1 : m0, vr[k], vi[k], xm[k]);
-            f2_cmac((k & 1) ? o1 : o0, vr[k], vi[k], xo[k]);
+            f2_cmac1((k & 1) ? m1 : m0, vr[k], vi[k], xm[k]);
+            f2_cmac1((k & 1) ? o1 : o0, vr[k], vi[k], xo[k]);
         }
         float kr = f2_lo(m0) + f2_lo(m1), ki = f2_hi(m0) + f2_hi(m1);
         const float sr_o = f2_lo(o0) + f2_lo(o1), si_o = f2_hi(o0) + f2_hi(o1);
@@ -337,13 +356,13 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
             ki += __shfl_xor_sync(0xffffffffu, ki, o);
         }
         float mr, mi;
-        hs_bvec(kr, ki, A_m, mr, mi);
+        hs_bvec_nb(kr, ki, A_m, mr, mi);
         const float orr = __shfl_xor_sync(0xffffffffu, mr, G / 2);
         const float oi = __shfl_xor_sync(0xffffffffu, mi, G / 2);
 #pragma unroll
-        for (int k = 0; k < SPL; ++k) f2_cmac(tt[k], mr, mi, xm[k]);
+        for (int k = 0; k < SPL; ++k) f2_cmac1(tt[k], mr, mi, xm[k]);
 #pragma unroll
-        for (int k = 0; k < SPL; ++k) f2_cmac(tt[k], orr, oi, xo[k]);
+        for (int k = 0; k < SPL; ++k) f2_cmac1(tt[k], orr, oi, xo[k]);
     };
 
     // End of chunk qi: flush, sum the 32 streams in a fixed order, reset, stage.
@@ -403,15 +422,98 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
         }
     };
 
+    // ---- pipelined per-pixel steps (PIPE) ----
+    // backward partial of one pixel over this lane's spots (two FFMA2 chains)
+    auto bwd = [&](const f2x (&x)[SPL], float &sr, float &si) {
+        f2x m0 = 0ull, m1 = 0ull;
+#pragma unroll
+        for (int k = 0; k < SPL; ++k) f2_cmac1((k & 1) ? m1 : m0, vr[k], vi[k], x[k]);
+        sr = f2_lo(m0) + f2_lo(m1);
+        si = f2_hi(m0) + f2_hi(m1);
+    };
+    // sum over the G lanes, transposed over (re, im): after the first
+    // exchange the low half of the group carries Re, the high half Im, so
+    // one value per lane goes through the remaining levels (commutative
+    // butterflies: every lane of a half ends with identical bits)
+    auto chain = [&](float sr, float si) {
+        float keep = lo ? sr : si;
+        keep += __shfl_xor_sync(0xffffffffu, lo ? si : sr, G / 2);
+#pragma unroll
+        for (int o = G / 4; o > 0; o >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, o);
+        return keep;
+    };
+    auto bfin = [&](float keep, float A, float &br, float &bi) {
+        const float other = __shfl_xor_sync(0xffffffffu, keep, G / 2);
+        hs_bvec_nb(lo ? keep : other, lo ? other : keep, A, br, bi);
+    };
+    auto fwd = [&](const f2x (&x)[SPL], float br, float bi) {
+#pragma unroll
+        for (int k = 0; k < SPL; ++k) f2_cmac1(tt[k], br, bi, x[k]);
+    };
+    // One chunk: entries (t, t+1) of a stream always lie in one run (runs are
+    // padded to even length and the two runs of a warp to the same length),
+    // so the row can only change at even t, warp-uniformly.  Per step the
+    // reduction of the previous pixel and the backward of the next one form
+    // one branch-free block; a row change re-runs the (already loaded)
+    // pixel's backward with the new V after the flush.
+    auto pipe_chunk = [&](uint32_t eb) {
+        int4 e;
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w) : "r"(eb));
+        rcur = e.x >> 16;
+        new_row(rcur);
+        f2x xa[SPL], xb[SPL];
+        float sr, si, A = __int_as_float(e.y);
+        load_x(e.x, xa);
+        bwd(xa, sr, si);
+#pragma unroll 1
+        for (int t = 0; t < P; t += 2) {
+            // pixel t (xa, partials sr/si) -> forward; pixel t+1 (same run) -> backward
+            load_x(e.z, xb);
+            const float A1 = __int_as_float(e.w);
+            float s1r, s1i, br, bi;
+            {
+                const float keep = chain(sr, si);
+                bwd(xb, s1r, s1i);
+                bfin(keep, A, br, bi);
+            }
+            fwd(xa, br, bi);
+            if (t + 2 < P) {
+                asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
+                             : "r"(eb + 8u * (t + 2)));
+                load_x(e.x, xa);
+                A = __int_as_float(e.y);
+                const float keep = chain(s1r, s1i);
+                bwd(xa, sr, si);
+                bfin(keep, A1, br, bi);
+                fwd(xb, br, bi);
+                const int r = e.x >> 16;
+                if (r != rcur) {  // warp-uniform
+                    flush();
+                    new_row(r);
+                    rcur = r;
+                    bwd(xa, sr, si);
+                }
+            } else {
+                bfin(chain(s1r, s1i), A1, br, bi);
+                fwd(xb, br, bi);
+            }
+        }
+    };
+
     for (int qi = 0; qi < nq; ++qi) {
         fetch_ent(qi + 2);
         // the next chunk's slab origin, read now (the previous chunk's last
         // barrier ordered the previous reads of s_next_c0 before this write)
         if (tid == 0 && qi + 1 < nq) s_next_c0 = __ldg(a.chunk_c0 + q0 + qi + 1);
+        if constexpr (PIPE) {
+            pipe_chunk((qi & 1) ? ent1 : ent0);
+        } else {
 #pragma unroll 1
-        for (int t = 0; t < P; t += 16) {
+            for (int t = 0; t < P; t += 16) {
 #pragma unroll
-            for (int u = 0; u < 16; u += 2) pair(qi, t + u);
+                for (int u = 0; u < 16; u += 2) pair(qi, t + u);
+            }
         }
         chunk_end(qi);
     }
@@ -423,5 +525,6 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
 
 typedef void (*SlabFn)(SlabArgs);
 SlabFn hs_select_slab(int ns, bool half);
+SlabFn hs_select_slab(int ns, bool half, bool pipe);
 
 }  // namespace hs
