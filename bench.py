@@ -505,7 +505,20 @@ def relaunch(args):
 CFG4_SPOTS, CFG4_ITERS = 1000, 30
 
 
-def cfg4_config(world):
+PANEL_W, PANEL_H = 1920, 1152   # the paper's SLM
+
+
+def cfg4_config(world, rect=False):
+    if rect:
+        return {"workload": "wgs_panel1920x1152_n1000_i30_rowsharded", "panel_px": [PANEL_H, PANEL_W],
+                "active_pixels": PANEL_W * PANEL_H, "spots": CFG4_SPOTS, "iterations": CFG4_ITERS,
+                "algorithm": "wgs",
+                "parallelism": f"row-sharded x{world} (group partials exchanged over peer memory "
+                               "each pass)" if world > 1 else "single GPU",
+                "pupil": "full rectangular 1920x1152 panel (build_panel), gaussian waist 6 mm, "
+                         "pitch 9.2 um, lambda 800 nm, f 20 mm, seed 0",
+                "foci": "uniform xy +-150 um, z +-50 um, spot seed 4, solver seed 0",
+                "l2": "inputs (tables, lists) L2-resident; one solve = 31 full passes"}
     return {"workload": "wgs_1152_n1000_i30_rowsharded", "side_px": SIDE, "spots": CFG4_SPOTS,
             "iterations": CFG4_ITERS, "algorithm": "wgs",
             "parallelism": f"row-sharded x{world} (one hologram cut at fold-group boundaries; "
@@ -515,12 +528,14 @@ def cfg4_config(world):
             "l2": "inputs (tables, lists) L2-resident; one solve = 31 full passes"}
 
 
-def run_cfg4(args):
-    """BASELINE configs[3]: WGS 1152^2 (square stand-in of the 1920x1152 panel),
-    N = 1000, I = 30 -- one hologram per step, row-sharded across the ranks
-    (distributed.solve_sharded's device path: peer-memory exchange of the
-    group partials, csrc/hs_xchg.cuh).  Strong scaling: the work per step is
-    fixed; value = holograms/s of the whole job."""
+def run_cfg4(args, rect=False):
+    """BASELINE configs[3]: WGS N = 1000, I = 30 on the 1152^2 circular
+    aperture (the parity stand-in) or, with rect=True, on the
+    full 1920x1152 panel itself (build_panel; throughput-only) -- one
+    hologram per step, row-sharded across the ranks (distributed.
+    solve_sharded's device path: peer-memory exchange of the group partials,
+    csrc/hs_xchg.cuh).  Strong scaling: the work per step is fixed; value =
+    holograms/s of the whole job."""
     import torch
     import paper_2003_05293_b200 as hs
     from paper_2003_05293_b200 import _lib
@@ -546,7 +561,7 @@ def run_cfg4(args):
         dist.all_gather_object(out, obj)
         return out
 
-    pupil = hs.build_pupil(SIDE)
+    pupil = hs.build_panel(PANEL_W, PANEL_H) if rect else hs.build_pupil(SIDE)
     m = pupil.active_count
     spots = hs.random_foci(CFG4_SPOTS, 4, xy=150e-6)
     plan = _lib.Plan(pupil, local)
@@ -599,14 +614,15 @@ def run_cfg4(args):
         return
     flop = 2 * FLOP_PER_PAIR_PASS * CFG4_SPOTS * m * (CFG4_ITERS + 1)
     ms = total_ms / args.steps
-    line = {"metric": "holograms/s (config 4: WGS 1152^2, N=1000, I=30, row-sharded)",
+    line = {"metric": "holograms/s (config 4: WGS 1920x1152 panel, N=1000, I=30, row-sharded)" if rect
+            else "holograms/s (config 4: WGS 1152^2, N=1000, I=30, row-sharded)",
             "value": 1e3 / ms, "unit": "holograms/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "ms_per_hologram": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
-            "data": "synthetic", "config": cfg4_config(world),
+            "data": "synthetic", "config": cfg4_config(world, rect),
             "achieved_tflops_fp32_equivalent": flop / (ms * 1e-3) / 1e12,
             "e": float(e[0]), "u": float(u[0]),
-            "reference_e_u": [0.906461, 0.158003], "clocks": clk,
+            **({} if rect else {"reference_e_u": [0.906461, 0.158003]}), "clocks": clk,
             "gpu_launches": plan.last_launch_count() * args.steps if world == 1 else
             (1 + 3 * (CFG4_ITERS + 1)) * args.steps,
             "shared_gpu": shared}
@@ -624,7 +640,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4"])
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4", "cfg4rect"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -632,8 +648,8 @@ def main():
         sys.exit(relaunch(args))
     if args.impl == "reference":
         run_reference(args)
-    elif args.workload == "cfg4":
-        run_cfg4(args)
+    elif args.workload in ("cfg4", "cfg4rect"):
+        run_cfg4(args, rect=args.workload == "cfg4rect")
     else:
         run_ours(args)
 

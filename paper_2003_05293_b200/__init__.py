@@ -15,7 +15,7 @@ from .kernels import (DEFAULT_CHUNK, SpotCoefficients, SpotTables, forward_proje
                       reduce_complex, spot_tables, superpose, warm_up)
 from .metrics import (QualityReport, efficiency, quality_report, spot_intensities,
                       target_relative, uniformity)
-from .optics import (CompressionPlan, Hologram, Pupil, SpotSet, build_pupil, phase_of,
+from .optics import (CompressionPlan, Hologram, Pupil, SpotSet, build_panel, build_pupil, phase_of,
                      spot_phase, wrap_phase)
 from .solvers import (PlannedRun, SolverConfig, SolverTrace, StepRecord, WgsState,
                       budget_controller, cswgs, predict_ops, rebalance_weights, rs, solve,
