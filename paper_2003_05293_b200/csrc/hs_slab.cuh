@@ -44,6 +44,12 @@ constexpr int kSlabWarps = kSlabThreads / 32;
 constexpr int kSlabStreams = 32;                 // pixel streams per CTA
 constexpr int kSlabP = 32;                       // entries per stream per chunk
 constexpr int kSlabL = kSlabStreams * kSlabP;    // entries per chunk
+// Entries in shared memory: [2 chunks][32 streams][kSlabP]; odd streams
+// store entry t at t ^ 2, so the two streams of a warp read their entry
+// pairs (t, t+1) from different banks (one wavefront per warp instead of two)
+constexpr int kEntStride = kSlabP;
+constexpr int kEntBuf = kSlabStreams * kEntStride;  // one chunk's entries in smem
+__host__ __device__ constexpr int hs_ent_swz(int stream) { return (stream & 1) << 1; }
 constexpr int kSlabSmemBudget = 220 * 1024;      // dynamic smem cap per CTA
 constexpr int kBulkPiece = 32 * 1024;            // bytes per cp.async.bulk
 
@@ -61,8 +67,8 @@ struct SlabArgs {
 
 __host__ __device__ constexpr size_t hs_slab_fixed_bytes(int np)
 {
-    // per-stream E [32][np] float2 + entries [2][kSlabL] int2 + coef [np] float2
-    return (size_t)kSlabStreams * np * 8 + (size_t)2 * kSlabL * 8 + (size_t)np * 8;
+    // per-stream E [32][np] float2 + entries [2][32][kEntStride] int2 + coef [np] float2
+    return (size_t)kSlabStreams * np * 8 + (size_t)2 * kEntBuf * 8 + (size_t)np * 8;
 }
 
 // Widest slab whose gx rows fit next to the per-CTA scratch.
@@ -163,8 +169,8 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
 
     float2 *Xs = reinterpret_cast<float2 *>(sm4);                 // [sw][NP]
     float2 *Es = Xs + (size_t)a.sw * NP;                            // [32][NP]
-    int2 *Ent = reinterpret_cast<int2 *>(Es + kSlabStreams * NP);   // [2][kSlabL]
-    float2 *coef_s = reinterpret_cast<float2 *>(Ent + 2 * kSlabL);  // [NP]
+    int2 *Ent = reinterpret_cast<int2 *>(Es + kSlabStreams * NP);   // [2][32][kEntStride]
+    float2 *coef_s = reinterpret_cast<float2 *>(Ent + 2 * kEntBuf); // [NP]
     // lane's first complex in a table row: spot VEC g (stride VEC G per j)
     const uint32_t xs_a = hs_smem_addr(Xs) + 8u * VEC * g;
     const uint32_t es_a = hs_smem_addr(Es) + 8u * (stream * NP + VEC * g);
@@ -186,7 +192,11 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
     auto store_ent = [&](int qi) {
         if (qi < nq)
 #pragma unroll
-            for (int k = 0; k < EPL; ++k) Ent[(qi & 1) * kSlabL + gw * GPW * P + lane + 32 * k] = ent_reg[k];
+            for (int k = 0; k < EPL; ++k) {
+                const int i = lane + 32 * k;  // entry i of the warp's GPW streams
+                const int st = gw * GPW + i / P;
+                Ent[(qi & 1) * kEntBuf + st * kEntStride + ((i % P) ^ hs_ent_swz(st))] = ent_reg[k];
+            }
     };
     fetch_ent(0);
     store_ent(0);
@@ -304,9 +314,10 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
     __syncthreads();
     int rcur = -1;
     // smem address of this stream's entries in chunk buffer 0 / 1
-    const uint32_t ent0 = ent_a + 8u * (stream * P), ent1 = ent0 + 8u * kSlabL;
+    const uint32_t ent0 = ent_a + 8u * (stream * kEntStride), ent1 = ent0 + 8u * kEntBuf;
+    const uint32_t eswz = 8u * hs_ent_swz(stream);  // byte offset XOR of entry pairs
     int4 en;
-    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(en.x), "=r"(en.y), "=r"(en.z), "=r"(en.w) : "r"(ent0));
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(en.x), "=r"(en.y), "=r"(en.z), "=r"(en.w) : "r"(ent0 + eswz));
 
     // One pair-trip = two pixels per group (entries t, t+1 of a run; runs are
     // padded to even length, so both share the row).  Lanes g < G/2 finish
@@ -321,7 +332,8 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
         load_x(rc_o, xo);
         {   // next pair's entries (the next chunk's buffer after the last pair;
             // past the CTA's last chunk the read is stale and unused)
-            const uint32_t nxt = (t + 2 < P) ? ((qi & 1) ? ent1 : ent0) + 8u * (t + 2) : ((qi & 1) ? ent0 : ent1);
+            const uint32_t nxt = ((t + 2 < P) ? ((qi & 1) ? ent1 : ent0) + (8u * (t + 2) ^ eswz)
+                                              : ((qi & 1) ? ent0 : ent1) + eswz);
             asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(en.x), "=r"(en.y), "=r"(en.z), "=r"(en.w)
                          : "r"(nxt));
@@ -458,7 +470,7 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
     // pixel's backward with the new V after the flush.
     auto pipe_chunk = [&](uint32_t eb) {
         int4 e;
-        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w) : "r"(eb));
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w) : "r"(eb + eswz));
         rcur = e.x >> 16;
         new_row(rcur);
         f2x xa[SPL], xb[SPL];
@@ -480,7 +492,7 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
             if (t + 2 < P) {
                 asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
-                             : "r"(eb + 8u * (t + 2)));
+                             : "r"(eb + (8u * (t + 2) ^ eswz)));
                 load_x(e.x, xa);
                 A = __int_as_float(e.y);
                 const float keep = chain(s1r, s1i);
