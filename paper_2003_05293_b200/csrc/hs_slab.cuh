@@ -288,14 +288,32 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
             sts_vec(es_a + 8u * VEC * G * j, e);
         }
     };
+    // Half-chunk CTAs (small batches: 8 warps per SM, where the gy-row load
+    // latency at each run start is exposed, ncu long_sb) keep the next run's
+    // gy row in registers (gyn, row rnext), loaded a whole run ahead from the
+    // row hint in the list; whole-chunk CTAs have no registers to spare.
+    constexpr bool PREF = HALF;
+    float2 gyn[PREF ? SPL : 1];
+    int rnext = -1;
+    auto load_next = [&](int r) {
+        if constexpr (PREF) {
+            const float2 *yrow = Y + (int64_t)r * NP;
+#pragma unroll
+            for (int j = 0; j < NS; ++j)
+#pragma unroll
+                for (int h = 0; h < VEC; ++h) gyn[VEC * j + h] = __ldg(yrow + VEC * G * j + h);
+            rnext = r;
+        }
+    };
     auto new_row = [&](int r) {  // Y = gy[r], V = coef * Y
         const float2 *yrow = Y + (int64_t)r * NP;
+        const bool pre = PREF && rnext == r;
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
 #pragma unroll
             for (int h = 0; h < VEC; ++h) {
                 const int k = VEC * j + h;
-                const float2 q = __ldg(yrow + VEC * G * j + h);
+                const float2 q = pre ? gyn[PREF ? k : 0] : __ldg(yrow + VEC * G * j + h);
                 const float2 w = hs_lds2(cf_a + 8u * (VEC * G * j + h));
                 yr_[k] = q.x;
                 yi_[k] = q.y;
@@ -344,10 +362,13 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
             new_row(r);
             rcur = r;
             // the second entry's row bits carry the row of this stream's next
-            // run: pull that gy row into L1 now, a run ahead of new_row
+            // run: load it a run ahead of new_row (PREF), else pull it into L1
             const int rn = e.z >> 16;
-            if (rn != r && g < NS + 1)
+            if constexpr (PREF) {
+                if (rn != r) load_next(rn);
+            } else if (rn != r && g < NS + 1) {
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(Yrow0 + (int64_t)rn * NP + min(16 * g, NP - 1)));
+            }
         }
         // backward partials of both pixels over this lane's spots (FFMA2)
         f2x m0 = 0ull, m1 = 0ull, o0 = 0ull, o1 = 0ull;

@@ -303,11 +303,13 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     const int grow = r0 + row;
     const bool row_in = grow < a.side;
 
-    // ---- backward X' loads: thread (column c = tid / 2, spot quad kq = tid % 2)
-    // of threads < 128 loads spots 8 ks + 4 kq .. + 4 of gx[c0 + c]; two
-    // k-steps in flight
+    // ---- backward X' loads: thread (column c = tid % 64, spot quad kq =
+    // (tid / 64) % 2) of warps 4-7 loads spots 8 ks + 4 kq .. + 4 of
+    // gx[c0 + c]; two k-steps in flight.  A warp's 32 threads hold 32
+    // consecutive columns of one spot quad, so each of its X' plane stores
+    // is 512 contiguous bytes (4 wavefronts, no bank conflicts)
     const bool xb_on = tid >= kUThreads - 2 * kUC;  // warps 4-7 (warp 0 issues the MMAs)
-    const int xb_c = (tid >> 1) & (kUC - 1), xb_kq = tid & 1;
+    const int xb_c = tid & (kUC - 1), xb_kq = (tid >> 6) & 1;
     const float4 *xb_src = reinterpret_cast<const float4 *>(gx + (int64_t)min(c0 + xb_c, a.side - 1) * a.np);
     float4 xq[2], xn[2];  // k-step ks, ks + 1
     auto load_b = [&](int ks, float4 (&d)[2]) {

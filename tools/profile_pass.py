@@ -24,6 +24,8 @@ ap.add_argument("--batch", type=int, default=32)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--spots", type=int, default=100)
 ap.add_argument("--solve", action="store_true")
+ap.add_argument("--alg", default="cswgs", choices=["cswgs", "wgs"])
+ap.add_argument("--iters", type=int, default=20)
 args = ap.parse_args()
 
 pupil = hs.build_pupil(1152)
@@ -32,9 +34,11 @@ plan = _lib.Plan(pupil, 0)
 sets = [hs.random_foci(args.spots, 1000 + k) for k in range(args.batch)]
 plan.set_spots(sets)
 th = np.stack([np.random.default_rng(k).random(args.spots) * 2 * math.pi for k in range(args.batch)])
-plan.solve(_lib.ALG_CSWGS, 20, subset, th)
+alg = _lib.ALG_CSWGS if args.alg == "cswgs" else _lib.ALG_WGS
+sub = subset if args.alg == "cswgs" else pupil.active_count
+plan.solve(alg, args.iters, sub, th)
 if args.solve:
-    plan.solve(_lib.ALG_CSWGS, 20, subset, th)
+    plan.solve(alg, args.iters, sub, th)
 else:
     ms, pairs = plan.time_kernel(args.which, subset, reps=args.reps)
     print(f"which={args.which} batch={args.batch} ms/launch={ms:.4f} pairs={pairs:.3e} "
