@@ -5,13 +5,15 @@
 // atan2's +-pi_f32 wrap to -+pi_f32 +- 2 pi exactly as hs_phase_f64 does on
 // the device, so the result is bit-identical to a device-side f64 store while
 // the device->host copy moves 4 instead of 8 bytes per pixel.  Runs on all
-// host threads with non-temporal stores (tools/widen_probe.c: 3.7 ms per
-// 33.4 M pixels on the B200 box's 16 cores).
+// host threads (a persistent pool) with non-temporal stores
+// (tools/widen_probe.c: 3.7 ms per 33.4 M pixels on the B200 box's 16 cores).
 #include <immintrin.h>
 #include <stdint.h>
 #include <stdlib.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -56,33 +58,106 @@ __attribute__((target("avx2"))) void widen_avx2(const float *src, double *dst, i
     _mm_sfence();
 }
 
-}  // namespace
+// Persistent widening workers: one job at a time (the slot's widen stream
+// runs its host functions in order), split into equal parts; the calling
+// thread (the CUDA driver's host-function thread) takes part 0.  Spawning
+// threads per call cost ~0.3 ms per chunk; waking parked workers costs a
+// few microseconds, so a download can be widened in small chunks while they
+// are still in the last-level cache.
+class WidenPool {
+  public:
+    explicit WidenPool(unsigned nt) : nt_(nt)
+    {
+        for (unsigned t = 1; t < nt_; ++t) workers_.emplace_back([this, t] { loop(t); });
+    }
+    ~WidenPool()
+    {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto &w : workers_) w.join();
+    }
+    unsigned threads() const { return nt_; }
+    void run(const float *src, double *dst, int64_t n, unsigned parts)
+    {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            src_ = src;
+            dst_ = dst;
+            n_ = n;
+            parts_ = parts;
+            pending_ = parts - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        part(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [this] { return pending_ == 0; });
+    }
 
-extern "C" void hs_widen_phases(const float *src, double *dst, int64_t n)
+  private:
+    void part(unsigned t)
+    {
+        const int64_t per = (n_ + parts_ - 1) / parts_;
+        const int64_t lo = std::min<int64_t>(n_, (int64_t)t * per), hi = std::min<int64_t>(n_, lo + per);
+        if (hi > lo) widen_run(src_ + lo, dst_ + lo, hi - lo);
+    }
+    void loop(unsigned t)
+    {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            const bool mine = t < parts_;
+            lk.unlock();
+            if (!mine) continue;
+            part(t);
+            lk.lock();
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    static void widen_run(const float *src, double *dst, int64_t n)
+    {
+        static const bool avx2 = __builtin_cpu_supports("avx2");
+        if (avx2) widen_avx2(src, dst, n);
+        else widen_scalar(src, dst, n);
+    }
+    unsigned nt_;
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+    const float *src_ = nullptr;
+    double *dst_ = nullptr;
+    int64_t n_ = 0;
+    unsigned parts_ = 1, pending_ = 0;
+};
+
+unsigned widen_threads()
 {
-    const bool avx2 = __builtin_cpu_supports("avx2");
     static const unsigned env_nt = getenv("HS_WIDEN_THREADS") ? (unsigned)atoi(getenv("HS_WIDEN_THREADS")) : 0;
     // all cores but two: the solve's host thread and the CUDA driver's own
     // threads keep running beside the widening (14 of 16 beat 16 of 16)
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    unsigned nt = env_nt ? env_nt : (hw > 4 ? hw - 2 : hw);
-    const int64_t min_per = 1 << 18;
-    nt = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, n / min_per));
-    auto run = [&](int64_t lo, int64_t hi) {
-        if (avx2) widen_avx2(src + lo, dst + lo, hi - lo);
-        else widen_scalar(src + lo, dst + lo, hi - lo);
-    };
-    if (nt <= 1) {
-        run(0, n);
+    return env_nt ? env_nt : (hw > 4 ? hw - 2 : hw);
+}
+
+}  // namespace
+
+extern "C" void hs_widen_phases(const float *src, double *dst, int64_t n)
+{
+    static WidenPool pool(widen_threads());  // created on first use, lives for the process
+    const int64_t min_per = 1 << 16;
+    const unsigned parts = (unsigned)std::min<int64_t>(pool.threads(), std::max<int64_t>(1, n / min_per));
+    if (parts <= 1) {
+        if (__builtin_cpu_supports("avx2")) widen_avx2(src, dst, n);
+        else widen_scalar(src, dst, n);
         return;
     }
-    std::vector<std::thread> pool;
-    pool.reserve(nt - 1);
-    const int64_t per = (n + nt - 1) / nt;
-    for (unsigned t = 1; t < nt; ++t) {
-        const int64_t lo = std::min<int64_t>(n, t * per), hi = std::min<int64_t>(n, lo + per);
-        pool.emplace_back(run, lo, hi);
-    }
-    run(0, std::min<int64_t>(n, per));
-    for (auto &th : pool) th.join();
+    pool.run(src, dst, n, parts);
 }

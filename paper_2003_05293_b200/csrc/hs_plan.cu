@@ -58,7 +58,7 @@ int fail(int code, const char *fmt, ...)
 
 constexpr int kColBlock = 64;  // dense layout: columns per CTA chunk
 constexpr int kSplitBatch = 16;  // batches >= this record two graph branches (record_solve)
-constexpr int kWidenChunks = 4;     // pieces of a phase-code download widened as they land
+constexpr int kWidenChunksMax = 32; // pieces of a phase-code download widened as they land (HS_WIDEN_CHUNKS)
 constexpr int kMaxSpots32 = 1024;   // largest n of the fp32 pixel kernels (G = 32 lanes x NL = 32)
 constexpr int kMaxSpots = 4096;     // largest n overall (fp64 passes: the fold keeps 32 B per spot in smem)
 // precision "auto": fp64 passes when the smallest pixel set a solve projects
@@ -220,12 +220,13 @@ struct hs_plan {
         const float *src;
         double *dst;
         int64_t n;
-    } widen_job[2][4];                    // [slot][chunk]
+    } widen_job[2][kWidenChunksMax];      // [slot][chunk]
+    int widen_chunks = 8;
     unsigned char *d_raster = nullptr;      // [cap_batch][side][side] SLM gray rasters
     int out_slot = 0, next_slot = 0;
     cudaStream_t copy_stream = nullptr;     // D2H of phases, overlapped with solves
     cudaStream_t widen_stream[2] = {nullptr, nullptr};  // host widening of a slot's codes
-    cudaEvent_t landed[2][5] = {};                       // a slot's code chunks (+ f64 part) reached the host
+    cudaEvent_t landed[2][kWidenChunksMax + 1] = {};     // a slot's code chunks (+ f64 part) reached the host
     double e2e_f64_frac = 0.375;          // hs_solve_host: share of patterns shipped as f64 (HS_E2E_F64_FRAC)
     cudaEvent_t solved[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
     double *d_trace_w = nullptr, *d_trace_m = nullptr;
@@ -1219,7 +1220,7 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
     CUDA_TRY(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
         CUDA_TRY(cudaStreamCreateWithFlags(&p->widen_stream[k], cudaStreamNonBlocking));
-        for (int q = 0; q <= kWidenChunks; ++q)
+        for (int q = 0; q <= kWidenChunksMax; ++q)
             CUDA_TRY(cudaEventCreateWithFlags(&p->landed[k][q], cudaEventDisableTiming));
     }
     CUDA_TRY(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
@@ -1259,6 +1260,7 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
     CUDA_TRY(cudaMemcpy(p->d_axis, axis, sizeof(double) * side, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(p->d_amp64, amplitude, sizeof(double) * m, cudaMemcpyHostToDevice));
     if (const char *env = getenv("HS_E2E_F64_FRAC")) p->e2e_f64_frac = std::min(1.0, std::max(0.0, atof(env)));
+    if (const char *env = getenv("HS_WIDEN_CHUNKS")) p->widen_chunks = std::min(kWidenChunksMax, std::max(1, atoi(env)));
     if (const char *env = getenv("HS_PRECISION")) {
         if (!strcmp(env, "fp32")) p->precision_mode = HS_PREC_FP32;
         else if (!strcmp(env, "fp64")) p->precision_mode = HS_PREC_FP64;
@@ -1366,7 +1368,7 @@ void hs_plan_destroy(hs_plan *p)
     cudaStreamDestroy(p->copy_stream);
     for (int k = 0; k < 2; ++k) {
         cudaStreamDestroy(p->widen_stream[k]);
-        for (int q = 0; q <= kWidenChunks; ++q) cudaEventDestroy(p->landed[k][q]);
+        for (int q = 0; q <= kWidenChunksMax; ++q) cudaEventDestroy(p->landed[k][q]);
     }
     cudaStreamDestroy(p->stream2);
     cudaStreamDestroy(p->stream3);
@@ -1871,7 +1873,7 @@ int hs_solve_host_async(hs_plan *p, int alg, int iters, int64_t subset, int batc
         //  * patterns [0, nb64): widened to f64 on the device (hs_widen_codes,
         //    bit-identical) and copied as f64 into the caller's buffer;
         //  * patterns [nb64, batch): 4-byte codes copied to pinned staging in
-        //    kWidenChunks pieces, each widened on the host threads (a host
+        //    widen_chunks pieces, each widened on the host threads (a host
         //    function on the slot's widen stream) as soon as it lands.
         // Both overlap the next call's solve.
         const int nb64 = (int)std::lround(p->e2e_f64_frac * batch);
@@ -1883,8 +1885,9 @@ int hs_solve_host_async(hs_plan *p, int alg, int iters, int64_t subset, int batc
         }
         CUDA_TRY(cudaEventRecord(p->solved[slot], p->stream));
         CUDA_TRY(cudaStreamWaitEvent(p->copy_stream, p->solved[slot], 0));
-        for (int q = 0; q < kWidenChunks && c32 > 0; ++q) {
-            const size_t lo = c64 + c32 * q / kWidenChunks, hi = c64 + c32 * (q + 1) / kWidenChunks;
+        const int nwc = p->widen_chunks;
+        for (int q = 0; q < nwc && c32 > 0; ++q) {
+            const size_t lo = c64 + c32 * q / nwc, hi = c64 + c32 * (q + 1) / nwc;
             CUDA_TRY(cudaMemcpyAsync(p->h_stage32[slot] + lo, p->d_out32[slot] + lo, sizeof(float) * (hi - lo),
                                      cudaMemcpyDeviceToHost, p->copy_stream));
             CUDA_TRY(cudaEventRecord(p->landed[slot][q], p->copy_stream));
@@ -1895,8 +1898,8 @@ int hs_solve_host_async(hs_plan *p, int alg, int iters, int64_t subset, int batc
         if (c64 > 0)
             CUDA_TRY(cudaMemcpyAsync(phase, p->d_out[slot], sizeof(double) * c64, cudaMemcpyDeviceToHost,
                                      p->copy_stream));
-        CUDA_TRY(cudaEventRecord(p->landed[slot][kWidenChunks], p->copy_stream));
-        CUDA_TRY(cudaStreamWaitEvent(p->widen_stream[slot], p->landed[slot][kWidenChunks], 0));
+        CUDA_TRY(cudaEventRecord(p->landed[slot][kWidenChunksMax], p->copy_stream));
+        CUDA_TRY(cudaStreamWaitEvent(p->widen_stream[slot], p->landed[slot][kWidenChunksMax], 0));
         CUDA_TRY(cudaEventRecord(p->copied[slot], p->widen_stream[slot]));
     } else {
         if (phase)
