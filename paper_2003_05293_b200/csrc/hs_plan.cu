@@ -222,6 +222,8 @@ struct hs_plan {
         int64_t n;
     } widen_job[2][kWidenChunksMax];      // [slot][chunk]
     int widen_chunks = 8;
+    unsigned long long *d_trace = nullptr;  // HS_UMMA_TRACE probe buffer
+    bool trace_next = false;
     unsigned char *d_raster = nullptr;      // [cap_batch][side][side] SLM gray rasters
     int out_slot = 0, next_slot = 0;
     cudaStream_t copy_stream = nullptr;     // D2H of phases, overlapped with solves
@@ -822,6 +824,10 @@ int launch_tile(hs_plan *p, bool write, const UpdArgs &u, double *phase_out, int
     a.raster = raster ? raster + (int64_t)p->view0 * p->side * p->side : nullptr;
     a.f = fold_args(p, ts.n, u, lo, hi);
     a.n = p->n;
+    if (p->trace_next) {
+        a.trace = p->d_trace;
+        p->trace_next = false;
+    }
     if (hi <= lo) return HS_OK;
     dim3 grid(hi - lo, p->batch);
     if (ts.umma) {
@@ -2315,6 +2321,19 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
     CUDA_TRY(cudaEventCreate(&e0));
     CUDA_TRY(cudaEventCreate(&e1));
     const UpdArgs u = upd_args(p, ACT_FIELDS);
+    if (which == 0 && getenv("HS_UMMA_TRACE")) {  // timing probe of one tcgen05 CTA
+        if ((rc = dalloc(&p->d_trace, 128))) return rc;
+        CUDA_TRY(cudaMemset(p->d_trace, 0, 128 * sizeof(unsigned long long)));
+        p->trace_next = true;
+        if ((rc = launch_tile(p, false, u, nullptr))) return rc;
+        CUDA_TRY(cudaStreamSynchronize(p->stream));
+        unsigned long long t[128];
+        CUDA_TRY(cudaMemcpy(t, p->d_trace, sizeof t, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "umma trace (cycles from CTA start):");
+        for (int i = 1; i < 128; ++i)
+            if (t[i]) fprintf(stderr, " %d:%lld", i, (long long)(t[i] - t[0]));
+        fprintf(stderr, "\n");
+    }
     auto once = [&]() -> int {
         if (which == 0) return launch_tile(p, false, u, nullptr);
         if (which == 2) return launch_tile(p, true, u, p->d_out[0]);  // final pass: f64 phase write

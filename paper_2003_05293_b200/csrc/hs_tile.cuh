@@ -49,6 +49,7 @@ struct TileArgs {
     unsigned char *raster;    // [B][side][side] SLM gray raster (WRITE, nullable)
     int64_t phase_stride;
     FoldArgs f;
+    unsigned long long *trace;  // timing probe of one CTA (hs_umma_kernel, HS_UMMA_TRACE), normally null
 };
 
 __host__ __device__ constexpr int hs_tile_kb(int n) { return (n + 1) & ~1; }

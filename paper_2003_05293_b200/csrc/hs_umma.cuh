@@ -47,6 +47,19 @@
 // per backward MMA, 7.5 KB per forward MMA); the per-tile CUDA-core work (b,
 // E reduce, fold) and the mbarrier waits make up the rest.
 //
+// Per-CTA timeline (HS_UMMA_TRACE=1 with hs_time_kernel: clock64 at fixed
+// points of one CTA, B = 32, round 2): prologue 2.0k cycles, 14 backward
+// k-steps 1.6-1.7k cycles each (the 6 MMAs need ~400), b 5k, 8 forward
+// k-steps ~1.7k each, E epilogue ~13k, fold ~3.5k: ~66k per tile per CTA.
+// The k-step cadence is the shared-memory data path: a kind::tf32 MMA with
+// K = 8 reads 4 KB of A and 4 KB of B per 64 MMA cycles -- 128 B/cycle, the
+// whole smem bandwidth -- and the TMA (16 KB), the operand stores (16 KB)
+// and the other CTA's MMAs share it.  Deeper rings (1 CTA per SM, TMA 3-4
+// steps ahead: HS_UMMA_RING=4..6), one elected arrival per warp and moving
+// the issuer's wait behind its issue left the cadence unchanged; fewer smem
+// bytes per MAC (kind::f16 with a 2-term fp16 split, A from TMEM) is what
+// would move it.
+//
 // Encodings (instruction descriptor, shared-memory descriptor, TMEM
 // st / ld, a_negate) are checked by tools/umma_probe.cu.
 #pragma once
@@ -63,8 +76,13 @@ constexpr int kUNPMax = 112;     // largest np run as one forward spot chunk (N 
 constexpr int kUNPC = 128;       // forward spot chunk for larger np (T: 2 x 128 TMEM columns)
 constexpr int kUThreads = 256;
 constexpr int kUTmem = 256;      // TMEM columns per CTA (two CTAs per SM)
-constexpr int kUA = 3;           // A ring: gy planes (backward, TMA) / b' (forward, threads)
-constexpr int kUB = 3;           // B ring: X' (backward, threads) / X^T planes (forward, TMA)
+#ifndef HS_UMMA_RING
+#define HS_UMMA_RING 3
+#endif
+constexpr int kUA = HS_UMMA_RING;  // A ring: gy planes (backward, TMA) / b' (forward, threads)
+constexpr int kUB = HS_UMMA_RING;  // B ring: X' (backward, threads) / X^T planes (forward, TMA)
+constexpr int kUD = kUA - 2;       // TMA prefetch distance (steps ahead of the MMA issue)
+constexpr int kUMinBlocks = kUA <= 3 ? 2 : 1;  // CTAs per SM the shared memory allows
 constexpr int kUAPl = kUR * kUF * 4;                // A plane [128][8] (4 KB)
 constexpr int kUASlot = 4 * kUAPl;                  // 16 KB
 // B slot: the backward's stacked X' planes ([Xr; Xi] and [-Xi; Xr], 128 rows,
@@ -261,7 +279,7 @@ __device__ __forceinline__ void hs_cmma(Mma mma, uint32_t dr, uint32_t di, AOp a
 }
 
 template <int NP, int WRITE>  // WRITE: 0 no phase, 1 f64 phases, 2 4-byte phase codes
-__global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel(const TileArgs a)
+__global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_umma_kernel(const TileArgs a)
 {
     static_assert(NP % 16 == 0 && (NP <= kUNPMax || NP == kUNPC), "forward N: np <= 112 or chunks of 128");
     constexpr int NCC = kUC / kUF;           // forward k-steps (8)
@@ -278,6 +296,12 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     hs_pdl_launch_next();
     const int pat = blockIdx.y;
     const int tile = a.f.chunk_base + blockIdx.x;
+    // timing probe: clock64 at fixed points of one CTA (tile 100, pattern 0)
+    const bool trc = a.trace && blockIdx.x == 100 && blockIdx.y == 0;
+    auto TR = [&](int who, int slot) {
+        if (trc && (int)threadIdx.x == who) a.trace[slot] = clock64();
+    };
+    TR(0, 0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = warp & 3, h = warp >> 2;  // TMEM lane quarter, column / spot half
     const int row = 32 * q + lane;          // tile row of this thread (TMEM lane)
@@ -347,7 +371,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     // j % 3, one step ahead (slot last used by j - 3).  Issued at step i after
     // the wait for MMA(i - 2).
     auto tma_ahead = [&](int i) {
-        const int j = i + 1;
+        const int j = i + kUD;
         if (j < ksteps) {
             bulk(sa + (j % kUA) * kUASlot, gyp + (int64_t)j * (kUASlot / 4), kUASlot, bar_af + 8 * (j % kUA));
         } else if (j < nsteps) {
@@ -358,14 +382,15 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     };
     if (tid == 0) {
         for (int i = 0; i < 2 * kUA + kUB; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar + 8 * i));
-        for (int i = 0; i < kUA; ++i)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_op + 8 * i), "n"(kUThreads));
+        for (int i = 0; i < kUA; ++i)  // one (elected) arrival per warp
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_op + 8 * i), "n"(kUThreads / 32));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        tma_ahead(-1);  // step 0's gy planes
+        for (int i = -kUD; i < 0; ++i) tma_ahead(i);  // steps 0 .. kUD-1
     }
     hs_tc_fence_before();
     __syncthreads();
     hs_tc_fence_after();
+    TR(0, 1);
     const uint32_t tm = s_tmem;
     const uint32_t tl = tm + ((uint32_t)(32 * q) << 16);  // this warp's lane quarter
 
@@ -399,13 +424,19 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
     // thread arrives on operand barrier j % 4 (completion j / 4), thread 0
     // waits for it.  No CTA-wide barrier per step: the other warps run ahead
     // until the MMA-done wait two steps back.
+    // Each thread fences its own writes into the async proxy; the warp
+    // converges and one lane arrives for it (256 single-thread arrivals on
+    // one barrier word serialised into ~1k cycles per step).
     auto publish = [&](int j) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         hs_tc_fence_before();
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_op + 8 * (j % kUA)) : "memory");
+        __syncwarp();
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_op + 8 * (j % kUA)) : "memory");
         if (tid == 0) {
             hs_mbar_wait(bar_op + 8 * (j % kUA), (uint32_t)(j / kUA) & 1u);
             hs_tc_fence_after();
+            if (j < 16) TR(0, 96 + j);
         }
     };
     auto mma_ss = [](uint32_t d, uint64_t av, uint64_t bv, uint32_t id, uint32_t acc) { hs_mma_ss(d, av, bv, id, acc); };
@@ -464,10 +495,13 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
         ++folded;
     };
     for (int ks = 0; ks < ksteps; ++ks) {
-        if (ks >= 2) wait_mma(ks - 2);  // A slot of ks + 2, B slots of ks + 1 and ks free
+        if (ks >= 2) wait_mma(ks - 2);  // A slot of ks + 1, B slot of ks free
+        if (ks < 16) TR(kUThreads - 2 * kUC, 64 + ks);
+        if (ks < 16) TR(0, 32 + ks);
         if (CH)  // groups whose last step is <= ks - 2 (group g is read before group g + 2 reuses its region)
             while (folded < (ks - 1) / KG) fold_group();
         if (tid == 0) tma_ahead(ks);
+        if (ks < 16) TR(0, 48 + ks);
         if (xb_on) {  // X' = coef_k gx[c][k], planes [64 columns][8 spots]: (c/8)*128 + (k/4)*1024 + (c%8)*16
             const int k = ks * kUF + 4 * xb_kq;
             const float2 w0 = coef_s[k], w1 = coef_s[k + 1], w2 = coef_s[k + 2], w3 = coef_s[k + 3];
@@ -495,11 +529,15 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
         xq[0] = xn[0];
         xq[1] = xn[1];
         load_b(ks + 2, xn);  // two k-steps in flight
+        if (ks < 16) TR(kUThreads - 2 * kUC, 80 + ks);
+
         publish(ks);
         if (tid == 0) {
             wait_tma(ks);  // gy planes landed
+            if (ks < 16) TR(0, 112 + ks);
             const uint32_t dr = CH ? tm + (uint32_t)(((ks / KG) & 1) * 128) : tm;
             issue_bwd(ks, dr, (CH ? ks % KG : ks) ? 1u : 0u);
+            if (ks < 16) TR(0, 2 + ks);
         }
     }
 
@@ -522,6 +560,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
         }
     }
     wait_mma(ksteps - 1);
+    TR(0, 18);
 
     if (CH)
         while (folded < (ksteps + KG - 1) / KG) fold_group();
@@ -582,6 +621,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
         }
     }
 
+    TR(0, 19);
     // ---- forward: T = b X ------------------------------------------------------
     // A slot: b' planes [128 rows][8 columns] (hs_uoff); B slot: X^T planes
     // [NP spots][8 columns] ((k/8)*128 + (c/4)*FLBO + (k%8)*16 + (c%4)*4), TMA
@@ -592,7 +632,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
 #pragma unroll
     for (int cc = 0; cc < NCC; ++cc) {
         const int j = ksteps + sc * NCC + cc;  // step
-        wait_mma(j - 2);             // A slot of j (last used by j - 4), B slot of j + 1 (j - 2) free
+        wait_mma(j - 2);             // A slot of j (last used by j - 3), B slot of j + 1 (j - 2) free
         if (tid == 0) tma_ahead(j);
         {   // b' (this thread's row, columns 4h .. 4h+3 of the k-step)
             float4 rh, rl, ih, il;
@@ -608,9 +648,11 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
         if (tid == 0) {
             wait_tma(j);  // X^T planes landed
             issue(j, tm, tm + NP, FLBO, FPL, idf, idfn, cc ? 1u : 0u);
+            if (sc == 0) TR(0, 20 + cc);
         }
     }
     wait_mma(ksteps + (sc + 1) * NCC - 1);
+    if (sc == 0) TR(0, 28);
 
     // ---- E_k = sum_r gy[r][k] T[r][k]: spots KH h .. KH (h+1) of the row, 16
     // at a time; each group of 16 (32 values) is transpose-reduced over the
@@ -701,11 +743,13 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : 2) hs_umma_kernel
         }
     }
     }  // spot chunks
+    TR(0, 29);
 
     hs_tc_fence_before();
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(kUTmem));
     if (a.f.u.act != ACT_NONE) hs_fold(a.f, pat, tile, reinterpret_cast<char *>(sbase));
+    TR(0, 30);
 }
 
 typedef void (*UmmaFn)(TileArgs);

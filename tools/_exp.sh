@@ -1,8 +1,4 @@
-# scratch driver for one gpurun experiment (the last one run is kept here)
-mkdir -p gpurun_out/r2
-rm -f gpurun_out/e2e_sweep.txt
-for c in 4 8 16; do for f in 0.25 0.375; do
-  echo "chunks $c frac $f" >> gpurun_out/e2e_sweep.txt
-  HS_WIDEN_CHUNKS=$c HS_E2E_F64_FRAC=$f timeout 300 python tools/e2e_probe.py --steps 20 2>&1 | grep -E "phase=True|widening 33" >> gpurun_out/e2e_sweep.txt
-done; done
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -k pipelined > gpurun_out/pipe_test.txt 2>&1
+rm -f gpurun_out/ring.txt
+timeout 300 python tools/ab_time.py >> gpurun_out/ring.txt 2>&1
+HS_UMMA_TRACE=1 timeout 300 python tools/profile_pass.py --which 0 --batch 32 >> gpurun_out/ring.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_umma.py tests/test_gpu_parity.py tests/test_gpu_spot_chunks.py -q -x > gpurun_out/ring_tests.txt 2>&1
