@@ -1304,7 +1304,7 @@ int hs_plan_create(int device, int side, int64_t m, const int64_t *rows, const i
                 lo = std::min(lo, p->row_lo[r]);
                 hi = std::max(hi, p->row_hi[r]);
             }
-            for (int c0 = lo & ~7; c0 < hi; c0 += kUC) utiles.push_back((r0 << 16) | c0);  // X^T plane blocks of 8
+            for (int c0 = lo & ~(kUF - 1); c0 < hi; c0 += kUC) utiles.push_back((r0 << 16) | c0);  // X^T plane blocks of kUF
         }
         p->nutiles = (int32_t)utiles.size();
         if ((rc = dalloc(&p->d_amp_img, cells)) || (rc = dalloc(&p->d_idx_img, cells)) ||

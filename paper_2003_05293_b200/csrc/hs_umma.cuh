@@ -64,6 +64,8 @@
 // st / ld, a_negate) are checked by tools/umma_probe.cu.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "hs_kernels.cuh"
 #include "hs_tile.cuh"
 
@@ -71,7 +73,22 @@ namespace hs {
 
 constexpr int kUR = 128;         // tile rows (MMA M)
 constexpr int kUC = 64;          // tile columns
-constexpr int kUF = 8;           // spots / columns per stage (one MMA k-step)
+// Operand format.  kind::f16 (default): every operand is split x = hi + lo
+// into two fp16 values and each real product is hi*hi + hi*lo + lo*hi, fp32
+// accumulate -- 22-bit products like the tf32 split, but an f16 MMA has
+// twice the K of a tf32 MMA at the same cost: a shared-memory-operand MMA
+// takes ~118 cycles for N <= 128 either way (tools/mma_rate.cu), so the
+// MMA time per tile halves.  The fp16 lo of a value below 2^-2 is subnormal;
+// the split then keeps an absolute error <= 2^-25, against unit-scale
+// phasors and |S| ~ sum a_n that is below the fp32 pixel noise.
+// HS_UMMA_F16=0 builds the tf32 variant.
+#ifndef HS_UMMA_F16
+#define HS_UMMA_F16 1
+#endif
+constexpr bool kF16 = HS_UMMA_F16 != 0;
+constexpr int kUEB = kF16 ? 2 : 4;  // operand element bytes
+constexpr int kUF = 32 / kUEB;      // spots / columns per stage (one MMA k-step: 32 bytes of K)
+constexpr int kUQ = 16 / kUEB;      // elements per 16-byte core-matrix row
 constexpr int kUNPMax = 112;     // largest np run as one forward spot chunk (N = np)
 constexpr int kUNPC = 128;       // forward spot chunk for larger np (T: 2 x 128 TMEM columns)
 constexpr int kUThreads = 256;
@@ -83,11 +100,11 @@ constexpr int kUA = HS_UMMA_RING;  // A ring: gy planes (backward, TMA) / b' (fo
 constexpr int kUB = HS_UMMA_RING;  // B ring: X' (backward, threads) / X^T planes (forward, TMA)
 constexpr int kUD = kUA - 2;       // TMA prefetch distance (steps ahead of the MMA issue)
 constexpr int kUMinBlocks = kUA <= 3 ? 2 : 1;  // CTAs per SM the shared memory allows
-constexpr int kUAPl = kUR * kUF * 4;                // A plane [128][8] (4 KB)
+constexpr int kUAPl = kUR * 32;                     // A plane [128 rows][32 bytes of K] (4 KB)
 constexpr int kUASlot = 4 * kUAPl;                  // 16 KB
 // B slot: the backward's stacked X' planes ([Xr; Xi] and [-Xi; Xr], 128 rows,
 // 16 KB) or the X^T of one forward k-step (npc spots, <= 16 KB).
-__host__ __device__ constexpr int hs_umma_bslot(int) { return 4 * 2 * kUC * kUF * 4; }
+__host__ __device__ constexpr int hs_umma_bslot(int) { return 4 * 2 * kUC * 32; }
 
 __host__ __device__ constexpr size_t hs_umma_smem_bytes(int np)
 {
@@ -102,33 +119,80 @@ __host__ __device__ constexpr int hs_umma_npc(int np) { return np <= kUNPMax ? n
 __host__ __device__ constexpr int hs_umma_nsc(int np) { return (np + hs_umma_npc(np) - 1) / hs_umma_npc(np); }
 
 // Operand planes of one pattern (constant per table build):
-//   gy : [band][k-step][4][128 rows][8 spots]                  (A of the backward)
-//   X^T: [column block of 8][spot chunk][4][npc spots][8 columns] (B of the forward),
-//        ceil(side / 8) + 8 column blocks (the tail blocks are zero)
+//   gy : [band][k-step][4][128 rows][kUF spots]                      (A of the backward)
+//   X^T: [column block of kUF][spot chunk][4][npc spots][kUF columns] (B of the forward),
+//        ceil(side / kUF) + kUC / kUF column blocks (the tail blocks are zero)
 __host__ __device__ constexpr int64_t hs_umma_gy_floats(int side, int np)
 {
     return (int64_t)((side + kUR - 1) / kUR) * (np / kUF) * (kUASlot / 4);
 }
-__host__ __device__ constexpr int hs_umma_xblocks(int side) { return (side + 7) / 8 + 8; }
+__host__ __device__ constexpr int hs_umma_xblocks(int side) { return (side + kUF - 1) / kUF + kUC / kUF; }
 __host__ __device__ constexpr int64_t hs_umma_xblock_floats(int np)
 {
-    return (int64_t)hs_umma_nsc(np) * 4 * hs_umma_npc(np) * kUF;
+    return (int64_t)hs_umma_nsc(np) * 4 * hs_umma_npc(np) * 8;  // 4 planes x npc rows x 32 bytes
 }
 __host__ __device__ constexpr int64_t hs_umma_plane_floats(int side, int np)
 {
     return hs_umma_gy_floats(side, np) + (int64_t)hs_umma_xblocks(side) * hs_umma_xblock_floats(np);
 }
 
-// Offset (floats) of element (r, k) in a [128][8] K-major operand plane.
-__host__ __device__ constexpr int hs_uoff(int r, int k) { return r * 4 + (k >> 2) * 512 + (k & 3); }
+// Byte offset of element (r, k) in a [128 rows][kUF] K-major operand plane
+// (SWIZZLE_NONE core matrices: 8 rows x 16 bytes; K halves 2048 B apart).
+__host__ __device__ constexpr int hs_uoffb(int r, int k) { return r * 16 + (k / kUQ) * 2048 + (k % kUQ) * kUEB; }
 
-__device__ __forceinline__ void hs_split_store(float v, float *dst, int plane_floats)
+// hi/lo split of one value in the operand format; returns the raw bits
+__device__ __forceinline__ void hs_split1(float v, uint32_t &hb, uint32_t &lb)
+{
+    if constexpr (kF16) {
+        const __half h = __float2half_rn(v);
+        const __half l = __float2half_rn(v - __half2float(h));
+        hb = __half_as_ushort(h);
+        lb = __half_as_ushort(l);
+    } else {
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(v - __uint_as_float(hb)));
+    }
+}
+
+__device__ __forceinline__ void hs_put(unsigned char *p, uint32_t bits)
+{
+    if constexpr (kF16) *reinterpret_cast<unsigned short *>(p) = (unsigned short)bits;
+    else *reinterpret_cast<uint32_t *>(p) = bits;
+}
+
+__device__ __forceinline__ void hs_split_store(float v, unsigned char *dst, int plane_bytes)
 {
     uint32_t h, l;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(v - __uint_as_float(h)));
-    dst[0] = __uint_as_float(h);
-    dst[plane_floats] = __uint_as_float(l);
+    hs_split1(v, h, l);
+    hs_put(dst, h);
+    hs_put(dst + plane_bytes, l);
+}
+
+// hi/lo split of one 16-byte core-matrix row chunk (kUQ values), and its negation
+__device__ __forceinline__ void hs_split_chunk(const float *v, uint4 &hi, uint4 &lo)
+{
+    uint32_t hb[kUQ], lb[kUQ];
+#pragma unroll
+    for (int i = 0; i < kUQ; ++i) hs_split1(v[i], hb[i], lb[i]);
+    if constexpr (kF16) {
+        hi = make_uint4(hb[0] | hb[1] << 16, hb[2] | hb[3] << 16, hb[4] | hb[5] << 16, hb[6] | hb[7] << 16);
+        lo = make_uint4(lb[0] | lb[1] << 16, lb[2] | lb[3] << 16, lb[4] | lb[5] << 16, lb[6] | lb[7] << 16);
+    } else {
+        hi = make_uint4(hb[0], hb[1], hb[2], hb[3]);
+        lo = make_uint4(lb[0], lb[1], lb[2], lb[3]);
+    }
+}
+__device__ __forceinline__ uint4 hs_neg_chunk(uint4 v)
+{
+    constexpr uint32_t m = kF16 ? 0x80008000u : 0x80000000u;
+    return make_uint4(v.x ^ m, v.y ^ m, v.z ^ m, v.w ^ m);
+}
+
+// operand element -> float (the gy planes read back by the E epilogue)
+__device__ __forceinline__ float hs_opnd(uint32_t bits)
+{
+    if constexpr (kF16) return __half2float(__ushort_as_half((unsigned short)bits));
+    else return __uint_as_float(bits);
 }
 
 // gy / gx -> tf32 hi/lo planes {re_h, re_l, im_h, im_l} in the operand
@@ -140,30 +204,31 @@ static __global__ void hs_umma_prep_kernel(const float2 *__restrict__ gx, const 
     const int nks = np / kUF;
     const int ngy = (side + kUR - 1) / kUR * nks;
     const int pat = blockIdx.y;
-    float *base = planes + (int64_t)pat * plane_stride;
+    unsigned char *base = reinterpret_cast<unsigned char *>(planes + (int64_t)pat * plane_stride);
     if ((int)blockIdx.x < ngy) {
         const int band = blockIdx.x / nks, ks = blockIdx.x % nks;
-        float *dst = base + (int64_t)blockIdx.x * (kUASlot / 4);
+        unsigned char *dst = base + (int64_t)blockIdx.x * kUASlot;
         for (int i = threadIdx.x; i < kUR * kUF; i += blockDim.x) {
             const int r = i / kUF, k = i % kUF;
             const int grow = band * kUR + r;
             const float2 v = grow < side ? gy[(int64_t)pat * tab_stride + (int64_t)grow * np + ks * kUF + k]
                                          : make_float2(0.f, 0.f);
-            const int o = hs_uoff(r, k);
-            hs_split_store(v.x, dst + o, kUAPl / 4);
-            hs_split_store(v.y, dst + o + kUAPl / 2, kUAPl / 4);
+            const int o = hs_uoffb(r, k);
+            hs_split_store(v.x, dst + o, kUAPl);
+            hs_split_store(v.y, dst + o + 2 * kUAPl, kUAPl);
         }
     } else {
         const int nsc = hs_umma_nsc(np), npc = hs_umma_npc(np);
         const int cb = (blockIdx.x - ngy) / nsc, sc = (blockIdx.x - ngy) % nsc;
-        const int pl = npc * kUF;  // plane floats
-        float *dst = base + hs_umma_gy_floats(side, np) + (int64_t)(blockIdx.x - ngy) * 4 * pl;
+        const int pl = npc * 32;  // plane bytes
+        unsigned char *dst = base + 4 * hs_umma_gy_floats(side, np) + (int64_t)(blockIdx.x - ngy) * 4 * pl;
         for (int i = threadIdx.x; i < npc * kUF; i += blockDim.x) {
             const int k = i / kUF, c = i % kUF;
             const int gc = cb * kUF + c, gk = sc * npc + k;
             const float2 v = (gc < side && gk < np) ? gx[(int64_t)pat * tab_stride + (int64_t)gc * np + gk]
                                                     : make_float2(0.f, 0.f);
-            const int o = (k >> 3) * 32 + (c >> 2) * (npc / 8) * 32 + (k & 7) * 4 + (c & 3);
+            // K-major over columns: 8-spot groups 128 B apart (SBO), column halves at npc/8 * 128 (LBO)
+            const int o = (k >> 3) * 128 + (c / kUQ) * (npc / 8) * 128 + (k & 7) * 16 + (c % kUQ) * kUEB;
             hs_split_store(v.x, dst + o, pl);
             hs_split_store(v.y, dst + o + 2 * pl, pl);
         }
@@ -177,27 +242,38 @@ __device__ __forceinline__ uint64_t hs_sdesc(uint32_t addr, uint32_t lbo, uint32
            ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | ((uint64_t)1 << 46);  // sm100 version, no swizzle
 }
 
-// kind::tf32, f32 accumulate, A and B K-major
+// kind::tf32 (A/B format 2) or kind::f16 (fp16: format 0), f32 accumulate,
+// A and B K-major
 __host__ __device__ constexpr uint32_t hs_idesc_tf32(int n, bool neg)
 {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((neg ? 1u : 0u) << 13) | ((uint32_t)(n >> 3) << 17) |
-           ((uint32_t)(kUR >> 4) << 24);
+    return (1u << 4) | ((kF16 ? 0u : 2u) << 7) | ((kF16 ? 0u : 2u) << 10) | ((neg ? 1u : 0u) << 13) |
+           ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kUR >> 4) << 24);
 }
 
 // A from TMEM
 __device__ __forceinline__ void hs_mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc)
 {
-    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                 " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
-                 "r"(a), "l"(b), "r"(idesc), "r"(acc));
+    if constexpr (kF16)
+        asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                     " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+                     "r"(a), "l"(b), "r"(idesc), "r"(acc));
+    else
+        asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                     " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+                     "r"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
 // A from shared memory
 __device__ __forceinline__ void hs_mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc)
 {
-    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                 " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
-                 "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    if constexpr (kF16)
+        asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                     " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+                     "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    else
+        asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                     " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+                     "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
 __device__ __forceinline__ void hs_tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -282,8 +358,9 @@ template <int NP, int WRITE>  // WRITE: 0 no phase, 1 f64 phases, 2 4-byte phase
 __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_umma_kernel(const TileArgs a)
 {
     static_assert(NP % 16 == 0 && (NP <= kUNPMax || NP == kUNPC), "forward N: np <= 112 or chunks of 128");
-    constexpr int NCC = kUC / kUF;           // forward k-steps (8)
-    constexpr uint32_t FPL = NP * kUF * 4;   // forward X^T plane bytes
+    constexpr int NCC = kUC / kUF;           // forward k-steps (4 fp16 / 8 tf32)
+    constexpr int NG8 = kUC / 8;             // 8-column groups of a tile row (b phase)
+    constexpr uint32_t FPL = NP * 32;        // forward X^T plane bytes (= floats of one 4-plane block)
     constexpr uint32_t FLBO = (NP / 8) * 128;
     constexpr int KH = NP / 2;               // spots per thread in the E epilogue
     constexpr int kUBSlot = hs_umma_bslot(NP);
@@ -306,16 +383,16 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     const int q = warp & 3, h = warp >> 2;  // TMEM lane quarter, column / spot half
     const int row = 32 * q + lane;          // tile row of this thread (TMEM lane)
     const int packed = __ldg(a.tiles + tile);
-    const int r0 = packed >> 16, c0 = packed & 0xffff;  // c0: multiple of 8
+    const int r0 = packed >> 16, c0 = packed & 0xffff;  // c0: multiple of kUF
     const float2 *gx = a.gx + (int64_t)pat * a.tab_stride;
     const float *pbase = a.gyp + (int64_t)pat * a.gyp_stride;
     const float *gyp = pbase + (int64_t)(r0 / kUR) * (a.np / kUF) * (kUASlot / 4);
     // forward spot chunks of NP: one when np <= 112 (b dies before the E
     // reduce); chunks of 128 otherwise (b stays live: one CTA per SM, no spills)
     const int nsc = NP <= kUNPMax ? 1 : hs_umma_nsc(a.np);
-    const float *xtp = pbase + hs_umma_gy_floats(a.side, a.np) + (int64_t)(c0 / kUF) * nsc * (4 * NP * kUF);
+    const float *xtp = pbase + hs_umma_gy_floats(a.side, a.np) + (int64_t)(c0 / kUF) * nsc * FPL;
     const int n = a.n;
-    const int ksteps = (n + 7) / 8;          // backward k-steps (8 spots)
+    const int ksteps = (n + kUF - 1) / kUF;  // backward k-steps (kUF spots)
     const int nsteps = ksteps + nsc * NCC;   // step sequence: backward, then forward per spot chunk
 
     unsigned char *sbase = reinterpret_cast<unsigned char *>(((uintptr_t)smu + 127) & ~(uintptr_t)127);
@@ -327,20 +404,21 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     const int grow = r0 + row;
     const bool row_in = grow < a.side;
 
-    // ---- backward X' loads: thread (column c = tid % 64, spot quad kq =
-    // (tid / 64) % 2) of warps 4-7 loads spots 8 ks + 4 kq .. + 4 of
+    // ---- backward X' loads: thread (column c = tid % 64, K half kq =
+    // (tid / 64) % 2) of warps 4-7 loads the kUQ spots kUF ks + kUQ kq .. of
     // gx[c0 + c]; two k-steps in flight.  A warp's 32 threads hold 32
-    // consecutive columns of one spot quad, so each of its X' plane stores
+    // consecutive columns of one K half, so each of its X' plane stores
     // is 512 contiguous bytes (4 wavefronts, no bank conflicts)
     const bool xb_on = tid >= kUThreads - 2 * kUC;  // warps 4-7 (warp 0 issues the MMAs)
     const int xb_c = tid & (kUC - 1), xb_kq = (tid >> 6) & 1;
     const float4 *xb_src = reinterpret_cast<const float4 *>(gx + (int64_t)min(c0 + xb_c, a.side - 1) * a.np);
-    float4 xq[2], xn[2];  // k-step ks, ks + 1
-    auto load_b = [&](int ks, float4 (&d)[2]) {
+    constexpr int XV = kUQ / 2;  // float4 (two complex) per thread and k-step
+    float4 xq[XV], xn[XV];       // k-step ks, ks + 1
+    auto load_b = [&](int ks, float4 (&d)[XV]) {
         if (xb_on && ks < ksteps) {
-            const int k = ks * kUF + 4 * xb_kq;
-            d[0] = __ldg(xb_src + k / 2);
-            d[1] = __ldg(xb_src + k / 2 + 1);
+            const int k = ks * kUF + kUQ * xb_kq;
+#pragma unroll
+            for (int i = 0; i < XV; ++i) d[i] = __ldg(xb_src + k / 2 + i);
         }
     };
     load_b(0, xq);  // gx: an input of the whole solve
@@ -376,7 +454,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
             bulk(sa + (j % kUA) * kUASlot, gyp + (int64_t)j * (kUASlot / 4), kUASlot, bar_af + 8 * (j % kUA));
         } else if (j < nsteps) {
             const int f = j - ksteps;  // spot chunk f / 8, column block f % 8
-            bulk(sbb + (j % kUB) * kUBSlot, xtp + ((int64_t)(f % NCC) * nsc + f / NCC) * (4 * NP * kUF), 4 * FPL,
+            bulk(sbb + (j % kUB) * kUBSlot, xtp + ((int64_t)(f % NCC) * nsc + f / NCC) * FPL, 4 * FPL,
                  bar_bf + 8 * (j % kUB));
         }
     };
@@ -479,12 +557,12 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     auto fold_group = [&]() {
         const uint32_t rg = tl + (uint32_t)((folded & 1) * 128);
 #pragma unroll
-        for (int cc = 0; cc < NCC; cc += 2) {
+        for (int cc = 0; cc < NG8; cc += 2) {
             float sr[8], si[8];
-            hs_tc_ld4(rg + cc * kUF + 4 * h, sr);
-            hs_tc_ld4(rg + (cc + 1) * kUF + 4 * h, sr + 4);
-            hs_tc_ld4(rg + kUC + cc * kUF + 4 * h, si);
-            hs_tc_ld4(rg + kUC + (cc + 1) * kUF + 4 * h, si + 4);
+            hs_tc_ld4(rg + cc * 8 + 4 * h, sr);
+            hs_tc_ld4(rg + (cc + 1) * 8 + 4 * h, sr + 4);
+            hs_tc_ld4(rg + kUC + cc * 8 + 4 * h, si);
+            hs_tc_ld4(rg + kUC + (cc + 1) * 8 + 4 * h, si + 4);
             hs_tc_wait_ld();
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
@@ -502,32 +580,35 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
             while (folded < (ks - 1) / KG) fold_group();
         if (tid == 0) tma_ahead(ks);
         if (ks < 16) TR(0, 48 + ks);
-        if (xb_on) {  // X' = coef_k gx[c][k], planes [64 columns][8 spots]: (c/8)*128 + (k/4)*1024 + (c%8)*16
-            const int k = ks * kUF + 4 * xb_kq;
-            const float2 w0 = coef_s[k], w1 = coef_s[k + 1], w2 = coef_s[k + 2], w3 = coef_s[k + 3];
-            const float4 u0 = xq[0], u1 = xq[1];
-            const float xr0 = fmaf(w0.x, u0.x, -w0.y * u0.y), xi0 = fmaf(w0.x, u0.y, w0.y * u0.x);
-            const float xr1 = fmaf(w1.x, u0.z, -w1.y * u0.w), xi1 = fmaf(w1.x, u0.w, w1.y * u0.z);
-            const float xr2 = fmaf(w2.x, u1.x, -w2.y * u1.y), xi2 = fmaf(w2.x, u1.y, w2.y * u1.x);
-            const float xr3 = fmaf(w3.x, u1.z, -w3.y * u1.w), xi3 = fmaf(w3.x, u1.w, w3.y * u1.z);
-            float4 rh, rl, ih, il;
-            hs_split4(xr0, xr1, xr2, xr3, rh, rl);
-            hs_split4(xi0, xi1, xi2, xi3, ih, il);
-            // planes [128 rows][8 spots] (hs_uoff): B1 = [Xr; Xi], B2 = [-Xi; Xr]
+        if (xb_on) {  // X' = coef_k gx[c][k]: kUQ spots of column c, one 16-byte chunk per plane
+            const int k = ks * kUF + kUQ * xb_kq;
+            float xr[kUQ], xi[kUQ];
+#pragma unroll
+            for (int i = 0; i < kUQ; ++i) {
+                const float2 w = coef_s[k + i];
+                const float4 u = xq[i / 2];
+                const float ur = (i & 1) ? u.z : u.x, ui = (i & 1) ? u.w : u.y;
+                xr[i] = fmaf(w.x, ur, -w.y * ui);
+                xi[i] = fmaf(w.x, ui, w.y * ur);
+            }
+            uint4 rh, rl, ih, il;
+            hs_split_chunk(xr, rh, rl);
+            hs_split_chunk(xi, ih, il);
+            // planes [128 rows][kUF spots] (hs_uoffb): B1 = [Xr; Xi], B2 = [-Xi; Xr]
             unsigned char *d = sbase + kUA * kUASlot + (ks % kUB) * kUBSlot + xb_c * 16 + xb_kq * 2048;
             constexpr int R64 = kUC * 16;  // row 64
-            const float4 nih = make_float4(-ih.x, -ih.y, -ih.z, -ih.w), nil = make_float4(-il.x, -il.y, -il.z, -il.w);
-            *reinterpret_cast<float4 *>(d) = rh;
-            *reinterpret_cast<float4 *>(d + R64) = ih;
-            *reinterpret_cast<float4 *>(d + kUAPl) = rl;
-            *reinterpret_cast<float4 *>(d + kUAPl + R64) = il;
-            *reinterpret_cast<float4 *>(d + 2 * kUAPl) = nih;
-            *reinterpret_cast<float4 *>(d + 2 * kUAPl + R64) = rh;
-            *reinterpret_cast<float4 *>(d + 3 * kUAPl) = nil;
-            *reinterpret_cast<float4 *>(d + 3 * kUAPl + R64) = rl;
+            const uint4 nih = hs_neg_chunk(ih), nil = hs_neg_chunk(il);
+            *reinterpret_cast<uint4 *>(d) = rh;
+            *reinterpret_cast<uint4 *>(d + R64) = ih;
+            *reinterpret_cast<uint4 *>(d + kUAPl) = rl;
+            *reinterpret_cast<uint4 *>(d + kUAPl + R64) = il;
+            *reinterpret_cast<uint4 *>(d + 2 * kUAPl) = nih;
+            *reinterpret_cast<uint4 *>(d + 2 * kUAPl + R64) = rh;
+            *reinterpret_cast<uint4 *>(d + 3 * kUAPl) = nil;
+            *reinterpret_cast<uint4 *>(d + 3 * kUAPl + R64) = rl;
         }
-        xq[0] = xn[0];
-        xq[1] = xn[1];
+#pragma unroll
+        for (int i = 0; i < XV; ++i) xq[i] = xn[i];
         load_b(ks + 2, xn);  // two k-steps in flight
         if (ks < 16) TR(kUThreads - 2 * kUC, 80 + ks);
 
@@ -547,8 +628,8 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     float br[32], bi[32];
     const bool vec_amp = (a.side & 3) == 0;
 #pragma unroll
-    for (int cc = 0; cc < NCC; ++cc) {
-        const int c = c0 + cc * kUF + 4 * h;
+    for (int cc = 0; cc < NG8; ++cc) {
+        const int c = c0 + cc * 8 + 4 * h;
         if (vec_amp) {
             const float4 v = (row_in && c < a.side) ? __ldg(reinterpret_cast<const float4 *>(a.amp_img + prow + c))
                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -567,7 +648,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
 
     // ---- S -> b = A conj(S)/|S| (registers), phase write --------------------
 #pragma unroll
-    for (int cc = 0; cc < NCC; cc += 2) {
+    for (int cc = 0; cc < NG8; cc += 2) {
         float sr[8], si[8];
         if (CH) {
 #pragma unroll
@@ -576,17 +657,17 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
                 si[jj] = sacc[32 + 4 * cc + jj];
             }
         } else {
-            hs_tc_ld4(tl + cc * kUF + 4 * h, sr);
-            hs_tc_ld4(tl + (cc + 1) * kUF + 4 * h, sr + 4);
-            hs_tc_ld4(tl + kUC + cc * kUF + 4 * h, si);
-            hs_tc_ld4(tl + kUC + (cc + 1) * kUF + 4 * h, si + 4);
+            hs_tc_ld4(tl + cc * 8 + 4 * h, sr);
+            hs_tc_ld4(tl + (cc + 1) * 8 + 4 * h, sr + 4);
+            hs_tc_ld4(tl + kUC + cc * 8 + 4 * h, si);
+            hs_tc_ld4(tl + kUC + (cc + 1) * 8 + 4 * h, si + 4);
             hs_tc_wait_ld();
         }
         int dix[8];  // storage indices of the 8 pixels (WRITE), two aligned int4 when side % 4 == 0
         if (WRITE) {
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                const int c = c0 + (cc + u) * kUF + 4 * h;
+                const int c = c0 + (cc + u) * 8 + 4 * h;
                 if (vec_amp) {
                     const int4 v = (row_in && c < a.side) ? __ldg(reinterpret_cast<const int4 *>(a.idx_img + prow + c))
                                                           : make_int4(-1, -1, -1, -1);
@@ -604,7 +685,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
             const float A = br[i];
             hs_bvec_exact(sr[jj], si[jj], A, br[i], bi[i]);
             if (WRITE) {
-                const int c = c0 + (i / 4) * kUF + 4 * h + (i % 4);
+                const int c = c0 + (i / 4) * 8 + 4 * h + (i % 4);
                 if (row_in && c < a.side) {
                     const int32_t di = dix[jj];
                     if (di >= 0) {
@@ -623,8 +704,8 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
 
     TR(0, 19);
     // ---- forward: T = b X ------------------------------------------------------
-    // A slot: b' planes [128 rows][8 columns] (hs_uoff); B slot: X^T planes
-    // [NP spots][8 columns] ((k/8)*128 + (c/4)*FLBO + (k%8)*16 + (c%4)*4), TMA
+    // A slot: b' planes [128 rows][kUF columns] (hs_uoffb); B slot: X^T planes
+    // [NP spots][kUF columns] ((k/8)*128 + (c/kUQ)*FLBO + (k%8)*16 + (c%kUQ)*kUEB), TMA
     const uint32_t idf = hs_idesc_tf32(NP, false), idfn = hs_idesc_tf32(NP, true);
     float2 *out = a.f.partials + (int64_t)pat * a.f.part_stride + (int64_t)tile * a.np;
 #pragma unroll 1
@@ -634,15 +715,31 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
         const int j = ksteps + sc * NCC + cc;  // step
         wait_mma(j - 2);             // A slot of j (last used by j - 3), B slot of j + 1 (j - 2) free
         if (tid == 0) tma_ahead(j);
-        {   // b' (this thread's row, columns 4h .. 4h+3 of the k-step)
-            float4 rh, rl, ih, il;
-            hs_split4(br[4 * cc], br[4 * cc + 1], br[4 * cc + 2], br[4 * cc + 3], rh, rl);
-            hs_split4(bi[4 * cc], bi[4 * cc + 1], bi[4 * cc + 2], bi[4 * cc + 3], ih, il);
+        if constexpr (kF16) {  // b' (this thread's row): columns 4h .. 4h+3 of both 8-column K halves
+#pragma unroll
+            for (int qh = 0; qh < 2; ++qh) {
+                const int g = 2 * cc + qh;  // 8-column group of the row
+                uint32_t hb[8], lb[8];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    hs_split1(br[4 * g + jj], hb[jj], lb[jj]);
+                    hs_split1(bi[4 * g + jj], hb[4 + jj], lb[4 + jj]);
+                }
+                unsigned char *d = sbase + (j % kUA) * kUASlot + row * 16 + qh * 2048 + h * 8;
+                *reinterpret_cast<uint2 *>(d) = make_uint2(hb[0] | hb[1] << 16, hb[2] | hb[3] << 16);
+                *reinterpret_cast<uint2 *>(d + kUAPl) = make_uint2(lb[0] | lb[1] << 16, lb[2] | lb[3] << 16);
+                *reinterpret_cast<uint2 *>(d + 2 * kUAPl) = make_uint2(hb[4] | hb[5] << 16, hb[6] | hb[7] << 16);
+                *reinterpret_cast<uint2 *>(d + 3 * kUAPl) = make_uint2(lb[4] | lb[5] << 16, lb[6] | lb[7] << 16);
+            }
+        } else {  // b' (this thread's row, columns 4h .. 4h+3 of the k-step = K half h)
+            uint4 rh, rl, ih, il;
+            hs_split_chunk(&br[4 * cc], rh, rl);
+            hs_split_chunk(&bi[4 * cc], ih, il);
             unsigned char *d = sbase + (j % kUA) * kUASlot + row * 16 + h * 2048;
-            *reinterpret_cast<float4 *>(d) = rh;
-            *reinterpret_cast<float4 *>(d + kUAPl) = rl;
-            *reinterpret_cast<float4 *>(d + 2 * kUAPl) = ih;
-            *reinterpret_cast<float4 *>(d + 3 * kUAPl) = il;
+            *reinterpret_cast<uint4 *>(d) = rh;
+            *reinterpret_cast<uint4 *>(d + kUAPl) = rl;
+            *reinterpret_cast<uint4 *>(d + 2 * kUAPl) = ih;
+            *reinterpret_cast<uint4 *>(d + 3 * kUAPl) = il;
         }
         publish(j);  // (cc = 0: also orders the S / previous chunk's T reads before T is overwritten)
         if (tid == 0) {
@@ -669,15 +766,37 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
         for (int e = 0; e < 2; ++e) {  // k8 block e of the group
             if (16 * g + 8 * e < KH) {
                 // spots past np (last chunk's padding): any finite plane data, T is 0 there
-                const int blk = min(k0 + kk + 8 * e, a.np - kUF) / kUF;
-                const float4 *pb = reinterpret_cast<const float4 *>(gyp + (int64_t)blk * (kUASlot / 4)) + row;
+                const int sp = min(k0 + kk + 8 * e, a.np - 8);  // first of 8 spots (multiple of 8)
+                const int blk = sp / kUF;
+                if constexpr (kF16) {
+                    // the 8 spots are one K half of the block: one 16-byte chunk per plane
+                    const unsigned char *pb = reinterpret_cast<const unsigned char *>(gyp) +
+                                              (int64_t)blk * kUASlot + ((sp % kUF) / 8) * 2048 + row * 16;
+                    uint4 c[4];
 #pragma unroll
-                for (int hq = 0; hq < 2; ++hq) {
-                    // quad hq of block e -> d[e][2 hq] (re: hi + lo), d[e][2 hq + 1] (im)
-                    const float4 rh = __ldg(pb + hq * 128), rl = __ldg(pb + 256 + hq * 128);
-                    const float4 ih = __ldg(pb + 512 + hq * 128), il = __ldg(pb + 768 + hq * 128);
-                    d[e][2 * hq] = make_float4(rh.x + rl.x, rh.y + rl.y, rh.z + rl.z, rh.w + rl.w);
-                    d[e][2 * hq + 1] = make_float4(ih.x + il.x, ih.y + il.y, ih.z + il.z, ih.w + il.w);
+                    for (int pl = 0; pl < 4; ++pl) c[pl] = __ldg(reinterpret_cast<const uint4 *>(pb + pl * kUAPl));
+                    auto h2 = [](uint32_t w, int hi) { return hs_opnd(hi ? w >> 16 : w & 0xffffu); };
+#pragma unroll
+                    for (int hq = 0; hq < 2; ++hq) {  // spots 4 hq .. 4 hq + 3 -> d[e][2 hq] (re), d[e][2 hq + 1] (im)
+                        const uint32_t r0w = hq ? c[0].z : c[0].x, r1w = hq ? c[0].w : c[0].y;
+                        const uint32_t l0w = hq ? c[1].z : c[1].x, l1w = hq ? c[1].w : c[1].y;
+                        const uint32_t i0w = hq ? c[2].z : c[2].x, i1w = hq ? c[2].w : c[2].y;
+                        const uint32_t m0w = hq ? c[3].z : c[3].x, m1w = hq ? c[3].w : c[3].y;
+                        d[e][2 * hq] = make_float4(h2(r0w, 0) + h2(l0w, 0), h2(r0w, 1) + h2(l0w, 1),
+                                                   h2(r1w, 0) + h2(l1w, 0), h2(r1w, 1) + h2(l1w, 1));
+                        d[e][2 * hq + 1] = make_float4(h2(i0w, 0) + h2(m0w, 0), h2(i0w, 1) + h2(m0w, 1),
+                                                       h2(i1w, 0) + h2(m1w, 0), h2(i1w, 1) + h2(m1w, 1));
+                    }
+                } else {
+                    const float4 *pb = reinterpret_cast<const float4 *>(gyp + (int64_t)blk * (kUASlot / 4)) + row;
+#pragma unroll
+                    for (int hq = 0; hq < 2; ++hq) {
+                        // quad hq of block e -> d[e][2 hq] (re: hi + lo), d[e][2 hq + 1] (im)
+                        const float4 rh = __ldg(pb + hq * 128), rl = __ldg(pb + 256 + hq * 128);
+                        const float4 ih = __ldg(pb + 512 + hq * 128), il = __ldg(pb + 768 + hq * 128);
+                        d[e][2 * hq] = make_float4(rh.x + rl.x, rh.y + rl.y, rh.z + rl.z, rh.w + rl.w);
+                        d[e][2 * hq + 1] = make_float4(ih.x + il.x, ih.y + il.y, ih.z + il.z, ih.w + il.w);
+                    }
                 }
             }
         }
