@@ -108,9 +108,9 @@ __host__ __device__ constexpr int hs_umma_bslot(int) { return 4 * 2 * kUC * 32; 
 
 __host__ __device__ constexpr size_t hs_umma_smem_bytes(int np)
 {
-    // rings + 128 B alignment slack + E reduce scratch [2][8 warps][32] float + coef [np]
+    // rings + 128 B alignment slack + E reduce scratch [4 groups][8 warps][32] float + coef [np]
     return (size_t)kUA * kUASlot + (size_t)kUB * hs_umma_bslot(np <= kUNPMax ? np : kUNPC) + 128 +
-           2 * 8 * 32 * sizeof(float) + 8 * (size_t)np;
+           4 * 8 * 32 * sizeof(float) + 8 * (size_t)np;
 }
 
 // Forward spot chunk (the MMA N) and chunk count for a table width np:
@@ -398,9 +398,8 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     unsigned char *sbase = reinterpret_cast<unsigned char *>(((uintptr_t)smu + 127) & ~(uintptr_t)127);
     const uint32_t sb = hs_smem_addr(sbase);
     const uint32_t sa = sb, sbb = sb + kUA * kUASlot;  // A ring, B ring
-    float *red = reinterpret_cast<float *>(sbase + kUA * kUASlot + kUB * kUBSlot);  // [2][8][32]
-    float2 *coef_s = reinterpret_cast<float2 *>(red + 2 * 8 * 32);                  // [np]
-    int redbuf = 0;  // E reduce scratch buffer, alternating per group of 16 spots
+    float *red = reinterpret_cast<float *>(sbase + kUA * kUASlot + kUB * kUBSlot);  // [4][8][32]
+    float2 *coef_s = reinterpret_cast<float2 *>(red + 4 * 8 * 32);                  // [np]
     const int grow = r0 + row;
     const bool row_in = grow < a.side;
 
@@ -841,26 +840,26 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
                 v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
             }
         }
-        // lane l holds value index l (value 2 s + t = spot s, re/im t).  Two
-        // alternating buffers: one barrier per group (a buffer is rewritten
-        // two groups later, after the next group's barrier)
-        float *rb = red + redbuf * 256;
-        redbuf ^= 1;
-        rb[warp * 32 + lane] = v[0];
-        __syncthreads();
-        if (tid < 2 * 16) {  // (spot-half hq, spot s of the group)
-            const int hq = tid >> 4, s = tid & 15;
-            if (s < KQ && k0 + KH * hq + 16 * g + s < a.np) {
-                float x = 0.f, y = 0.f;
+        // lane l holds value index l (value 2 s + t = spot s, re/im t); each
+        // group has its own scratch row, so the groups' shuffle chains run
+        // back to back and one barrier serves all of them
+        red[(g * 8 + warp) * 32 + lane] = v[0];
+    }
+    __syncthreads();
+    for (int idx = tid; idx < NG * 2 * 16; idx += kUThreads) {  // (group g, spot-half hq, spot s)
+        const int g = idx >> 5, hq = (idx >> 4) & 1, s = idx & 15;
+        const int KQ = min(16, KH - 16 * g);
+        if (s < KQ && k0 + KH * hq + 16 * g + s < a.np) {
+            float x = 0.f, y = 0.f;
 #pragma unroll
-                for (int qq = 0; qq < 4; ++qq) {
-                    x += rb[(qq + 4 * hq) * 32 + 2 * s];
-                    y += rb[(qq + 4 * hq) * 32 + 2 * s + 1];
-                }
-                out[k0 + KH * hq + 16 * g + s] = make_float2(x, y);
+            for (int qq = 0; qq < 4; ++qq) {
+                x += red[(g * 8 + qq + 4 * hq) * 32 + 2 * s];
+                y += red[(g * 8 + qq + 4 * hq) * 32 + 2 * s + 1];
             }
+            out[k0 + KH * hq + 16 * g + s] = make_float2(x, y);
         }
     }
+    if (sc + 1 < nsc) __syncthreads();  // the next chunk's groups rewrite the scratch
     }  // spot chunks
     TR(0, 29);
 
