@@ -244,34 +244,38 @@ def run_reference(args):
 
 def umma_roofline(pupil, batch, n, ms):
     """Tensor-pipe roofline of the tcgen05 full pass (csrc/hs_umma.cuh):
-    executed tf32 MMA flops per launch (128-row x 64-column tiles over the
-    aperture's row bands, 12 MMAs per complex 8-deep k-step: 3-term hi/lo
-    split x 4 real products) against half the measured dense bf16 peak."""
+    executed kind::f16 MMA flops per launch (128-row x 64-column tiles over
+    the aperture's row bands; per complex 16-deep k-step 6 backward MMAs
+    (N = 128) and 12 forward MMAs (N = np): a 2-term fp16 hi/lo split, 3
+    products per real product) against the measured dense bf16 peak (fp16
+    runs at the bf16 rate)."""
     side = pupil.side_px
     rows = np.asarray(pupil.rows)
     cols = np.asarray(pupil.cols)
+    kuf = 16  # K per f16 MMA (columns / spots per k-step)
     tiles = 0
     for r0 in range(0, side, 128):
         sel = (rows >= r0) & (rows < r0 + 128)
         if sel.any():
-            lo, hi = int(cols[sel].min()) & ~7, int(cols[sel].max()) + 1
+            lo, hi = int(cols[sel].min()) & ~(kuf - 1), int(cols[sel].max()) + 1
             tiles += -(-(hi - lo) // 64)
     npad = -(-n // 16) * 16
-    ksteps = -(-n // 8)
-    flop = tiles * batch * 12 * 2 * 128 * 8 * (ksteps * 64 + 8 * npad)
+    ksteps = -(-n // kuf)
+    flop = tiles * batch * 2 * 128 * kuf * (6 * 128 * ksteps + 12 * (64 // kuf) * npad)
     peaks = {}
     ppath = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(ppath):
         peaks = json.load(open(ppath))
     bf16 = peaks.get("bf16_tflops")
-    peak = bf16 / 2 if bf16 else 1100.0
+    peak = bf16 if bf16 else 2250.0
     achieved = flop / (ms * 1e-3) / 1e12
-    return {"bound": "tensor", "executed_tf32_flop_per_launch": flop, "tiles_per_pattern": tiles,
+    return {"bound": "tensor", "executed_f16_flop_per_launch": flop, "tiles_per_pattern": tiles,
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense tf32 = half of bf16)"
-            if bf16 else "B200_PROFILING.md nominal dense tf32 1.1 PFLOP/s",
-            "note": "ncu: tensor pipe ~39% active, tensor-core shared-memory operand reads ~32%; "
-                    "the per-tile CUDA-core work (b, E reduce, fold) fills the rest"}
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense f16 = bf16 rate)"
+            if bf16 else "B200_PROFILING.md nominal dense bf16/fp16 2.25 PFLOP/s",
+            "note": "shared-memory-operand MMAs cost ~118 cycles each at N <= 128 (tools/mma_rate.cu: "
+                    "twice the ideal); per-tile timeline in csrc/hs_umma.cuh (HS_UMMA_TRACE): the "
+                    "b and E epilogues run serially with the MMAs inside a CTA"}
 
 
 def run_ours(args):
@@ -468,7 +472,7 @@ def run_ours(args):
                      "complex MAC, SURVEY 8(d)); units per launch = S * N * B",
                      "ms_per_launch": ms_win,
                      "step_share_estimate": n_win * ms_win / step_kernel_ms,
-                     "full_pass": {"kernel": "hs_umma_kernel<112> tcgen05 kind::tf32 (3-term split) "
+                     "full_pass": {"kernel": "hs_umma_kernel<112> tcgen05 kind::f16 (2-term fp16 split) "
                                              "128x64-pixel tiles",
                                    "ms_per_launch": ms_full,
                                    "final_pass_ms_per_launch": ms_final,
