@@ -38,6 +38,9 @@
 
 namespace hs {
 
+#ifndef HS_SLAB_L1PF
+#define HS_SLAB_L1PF 0  // 1: whole-chunk CTAs prefetch the next run's gy row into L1 (measured neutral)
+#endif
 constexpr int kSlabG = 16;                       // lanes per pixel (8 or 16)
 constexpr int kSlabThreads = 32 * kSlabG;        // 32 streams of kSlabG lanes
 constexpr int kSlabWarps = kSlabThreads / 32;
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
             const int rn = e.z >> 16;
             if constexpr (PREF) {
                 if (rn != r) load_next(rn);
-            } else if (rn != r && g < NS + 1) {
+            } else if (HS_SLAB_L1PF && rn != r && g < NS + 1) {
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(Yrow0 + (int64_t)rn * NP + min(16 * g, NP - 1)));
             }
         }

@@ -1,3 +1,2 @@
-mkdir -p gpurun_out/san
-timeout 900 compute-sanitizer --tool racecheck --print-limit 5 python tools/sanitize.py > gpurun_out/san/racecheck_f16.txt 2>&1; echo "rc=$?" >> gpurun_out/san/racecheck_f16.txt
-HS_LIB_PATH=abtest/tf32.so timeout 900 compute-sanitizer --tool racecheck --print-limit 5 python tools/sanitize.py > gpurun_out/san/racecheck_tf32.txt 2>&1; echo "rc=$?" >> gpurun_out/san/racecheck_tf32.txt
+rm -f gpurun_out/cpc.txt
+for c in 0 1 2 4 8 16; do echo "cpc $c" >> gpurun_out/cpc.txt; HS_SLAB_CPC=$c timeout 300 python tools/ab_time.py >> gpurun_out/cpc.txt 2>&1; done
