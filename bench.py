@@ -580,8 +580,7 @@ def run_cfg4(args, rect=False):
 
         def solve():
             plan.shard_begin(_lib.ALG_WGS, CFG4_ITERS, m, th, rank, world)
-            for j in range(CFG4_ITERS + 1):
-                plan.p2p_pass(j)
+            plan.p2p_solve()  # all passes as one captured graph (hs_shard_p2p_solve)
     else:
         def solve():
             plan.solve(_lib.ALG_WGS, CFG4_ITERS, m, th, want_fields=True, sync=False)
@@ -629,7 +628,7 @@ def run_cfg4(args, rect=False):
             "e": float(e[0]), "u": float(u[0]),
             **({} if rect else {"reference_e_u": [0.906461, 0.158003]}), "clocks": clk,
             "gpu_launches": plan.last_launch_count() * args.steps if world == 1 else
-            (1 + 3 * (CFG4_ITERS + 1)) * args.steps,
+            (2 + 3 * (CFG4_ITERS + 1)) * args.steps,
             "shared_gpu": shared}
     print(json.dumps(line), flush=True)
     if dist is not None:

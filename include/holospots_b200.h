@@ -247,6 +247,10 @@ int hs_shard_groups(hs_plan *plan, int pass, int *g_lo, int *g_hi, int *ngroups)
 int hs_shard_p2p_setup(hs_plan *plan, unsigned char *ipc_handle_out);
 int hs_shard_p2p_open(hs_plan *plan, const unsigned char *ipc_handles);
 int hs_shard_p2p_pass(hs_plan *plan, int pass);
+/* All passes of the begun sharded solve in one call: captured into a CUDA
+ * graph on first use (per algorithm, iterations, subset, batch, n, rank and
+ * world) and replayed; equal to calling hs_shard_p2p_pass for every pass. */
+int hs_shard_p2p_solve(hs_plan *plan);
 int hs_shard_p2p_close(hs_plan *plan);
 int hs_padded_spots(hs_plan *plan);
 

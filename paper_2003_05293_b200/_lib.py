@@ -48,7 +48,7 @@ EXPORTS = (
     "hs_last_launch_count", "hs_time_kernel", "hs_fma_peak", "hs_host_alloc",
     "hs_host_free", "hs_probe", "hs_solve_host_async", "hs_shard_begin", "hs_shard_pass",
     "hs_shard_update", "hs_padded_spots", "hs_shard_groups", "hs_raster", "hs_get_raster",
-    "hs_shard_p2p_setup", "hs_shard_p2p_open", "hs_shard_p2p_pass", "hs_shard_p2p_close",
+    "hs_shard_p2p_setup", "hs_shard_p2p_open", "hs_shard_p2p_pass", "hs_shard_p2p_solve", "hs_shard_p2p_close",
     "hs_set_precision", "hs_get_precision", "hs_get_tables", "hs_set_tables",
     "hs_debug_update", "hs_host_copy_split",
 )
@@ -108,6 +108,7 @@ def load():
             "hs_shard_p2p_setup": (I, [P, P]),
             "hs_shard_p2p_open": (I, [P, P]),
             "hs_shard_p2p_pass": (I, [P, I]),
+            "hs_shard_p2p_solve": (I, [P]),
             "hs_shard_p2p_close": (I, [P]),
             "hs_set_precision": (I, [P, I]),
             "hs_get_precision": (I, [P, ctypes.POINTER(I), ctypes.POINTER(I)]),
@@ -386,6 +387,10 @@ class Plan:
     def p2p_pass(self, j: int) -> None:
         """Enqueue pass j (chunk range + peer publish + gather/update); async."""
         check(load().hs_shard_p2p_pass(self.handle, j))
+
+    def p2p_solve(self) -> None:
+        """Every pass of the begun sharded solve as one captured CUDA graph."""
+        check(load().hs_shard_p2p_solve(self.handle))
 
     def p2p_close(self) -> None:
         check(load().hs_shard_p2p_close(self.handle))

@@ -260,8 +260,10 @@ struct hs_plan {
         double2 **d_xbuf = nullptr;       // [world] device array of xbuf pointers
         unsigned long long **d_flags = nullptr;
         int32_t *d_cnt = nullptr;
-        uint64_t epoch = 0;
+        unsigned long long *d_epoch = nullptr;  // [2]: epoch counter, base of the current solve
         bool open = false;
+        // captured p2p solves, keyed by (alg, iters, subset, batch, n, rank, world)
+        std::map<std::tuple<int, int, int64_t, int, int, int, int>, cudaGraphExec_t> graphs;
     } xchg;
     int64_t last_launches = 0;
     std::map<std::tuple<int, int, int64_t, int, int, int>, cudaGraphExec_t> graphs;
@@ -2068,7 +2070,8 @@ int hs_shard_p2p_setup(hs_plan *p, unsigned char *handle_out)
     memcpy(handle_out, &h, sizeof h);
     if ((rc = dalloc(&x.d_cnt, 1))) return rc;
     CUDA_TRY(cudaMemset(x.d_cnt, 0, sizeof(int32_t)));
-    x.epoch = 0;
+    if ((rc = dalloc(&x.d_epoch, 2))) return rc;
+    CUDA_TRY(cudaMemset(x.d_epoch, 0, 2 * sizeof(unsigned long long)));
     return HS_OK;
 }
 
@@ -2120,6 +2123,10 @@ int hs_shard_p2p_pass(hs_plan *p, int j)
     const bool last = (j == sh.passes - 1);
     const int mode = last ? (PM_BWD | PM_FWD | PM_WRITE) : (PM_BWD | PM_FWD);
     const UpdArgs none = upd_args(p, ACT_NONE);
+    if (j == 0) {  // epochs of this solve: base + 1 .. base + passes
+        hs_epoch_advance_kernel<<<1, 32, 0, p->stream>>>(x.d_epoch, x.d_epoch + 1, sh.passes);
+        CUDA_TRY(cudaGetLastError());
+    }
     if (kind == 0)
         rc = launch_tile(p, last, none, p->d_out[0], lo, hi);
     else
@@ -2140,7 +2147,8 @@ int hs_shard_p2p_pass(hs_plan *p, int j)
     a.world = sh.world;
     a.rank = sh.rank;
     a.slot = j & 1;
-    a.epoch = ++x.epoch;
+    a.epoch0 = x.d_epoch + 1;
+    a.pass = j;
     a.peer_xbuf = x.d_xbuf;
     a.peer_flags = x.d_flags;
     a.flags_local = (unsigned long long *)x.local;
@@ -2162,10 +2170,51 @@ int hs_shard_p2p_pass(hs_plan *p, int j)
     return HS_OK;
 }
 
+// All passes of the sharded solve begun by hs_shard_begin as one CUDA graph
+// (captured on first use per (algorithm, iterations, subset, batch, n, rank,
+// world), then replayed): the same kernels hs_shard_p2p_pass enqueues, with
+// the epochs taken from device memory, so nothing is enqueued per pass.
+int hs_shard_p2p_solve(hs_plan *p)
+{
+    auto &sh = p->shard;
+    auto &x = p->xchg;
+    if (!sh.active) return fail(HS_EINVAL, "hs_shard_begin first");
+    if (!x.open) return fail(HS_EINVAL, "hs_shard_p2p_open first");
+    int rc;
+    if ((rc = check_device(p))) return rc;
+    const auto key = std::make_tuple(sh.alg, sh.iters, sh.subset, p->batch, p->n, sh.rank, sh.world);
+    auto it = x.graphs.find(key);
+    if (it == x.graphs.end()) {
+        // host-side list building happens outside graph capture
+        const DevList *l;
+        if ((rc = get_dense(p, p->cfg.spw, &l))) return rc;
+        for (int j = 0; j < sh.passes; ++j) {
+            int kind, nch;
+            if ((rc = shard_pass_desc(p, j, &kind, &l, &nch))) return rc;
+        }
+        cudaGraph_t graph;
+        CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+        for (int j = 0; j < sh.passes && !rc; ++j) rc = hs_shard_p2p_pass(p, j);
+        cudaError_t ce = cudaStreamEndCapture(p->stream, &graph);
+        if (rc) return rc;
+        if (ce != cudaSuccess) return fail(HS_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+        cudaGraphExec_t exec;
+        ce = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) return fail(HS_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
+        it = x.graphs.emplace(key, exec).first;
+    }
+    CUDA_TRY(cudaGraphLaunch(it->second, p->stream));
+    sh.active = false;
+    return HS_OK;
+}
+
 int hs_shard_p2p_close(hs_plan *p)
 {
     auto &x = p->xchg;
     if (x.local) cudaStreamSynchronize(p->stream);
+    for (auto &g : x.graphs) cudaGraphExecDestroy(g.second);
+    x.graphs.clear();
     for (size_t r = 0; r < x.bases.size(); ++r)
         if (x.bases[r] && x.bases[r] != x.local) cudaIpcCloseMemHandle(x.bases[r]);
     x.bases.clear();
@@ -2174,6 +2223,7 @@ int hs_shard_p2p_close(hs_plan *p)
     dfree(x.d_xbuf);
     dfree(x.d_flags);
     dfree(x.d_cnt);
+    dfree(x.d_epoch);
     x.open = false;
     return HS_OK;
 }

@@ -38,7 +38,8 @@ struct XchgArgs {
     int32_t ngroups;            // all groups of the pass
     int32_t ngmax;              // group capacity of a slot
     int32_t world, rank, slot;
-    uint64_t epoch;
+    const unsigned long long *epoch0;  // device: epoch base of the current solve (hs_epoch_advance_kernel)
+    int32_t pass;                      // the pass publishes / waits for epoch *epoch0 + pass + 1
     double2 *const *peer_xbuf;  // [world] xbuf bases (slot 0), device pointers
     unsigned long long *const *peer_flags;  // [world] flags bases
     unsigned long long *flags_local;
@@ -70,6 +71,17 @@ __device__ __forceinline__ unsigned long long hs_ld_acquire_sys(const unsigned l
     return v;
 }
 
+// Start of a sharded solve: the passes of this solve publish epochs
+// base + 1 .. base + passes.  The epoch lives in device memory (not in the
+// kernel arguments) so a captured solve graph replays with fresh epochs.
+static __global__ void hs_epoch_advance_kernel(unsigned long long *ctr, unsigned long long *base, int passes)
+{
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        *base = *ctr;
+        *ctr += (unsigned long long)passes;
+    }
+}
+
 static __global__ void __launch_bounds__(128) hs_publish_kernel(const XchgArgs a)
 {
     const int grp = a.g_lo + blockIdx.x, pat = blockIdx.y, np = a.f.np;
@@ -95,7 +107,8 @@ static __global__ void __launch_bounds__(128) hs_publish_kernel(const XchgArgs a
             __threadfence_system();
             bool failed = false;   // any pattern of this rank failed: tell the peers
             for (int b = 0; b < a.batch; ++b) failed |= (*(volatile int32_t *)(a.f.u.status + b) != 0);
-            const unsigned long long v = a.epoch | (failed ? kXchgAbort : 0ull);
+            const unsigned long long epoch = *a.epoch0 + (unsigned long long)a.pass + 1ull;
+            const unsigned long long v = epoch | (failed ? kXchgAbort : 0ull);
             for (int r = 0; r < a.world; ++r) hs_st_release_sys(a.peer_flags[r] + a.rank, v);
         }
     }
@@ -110,10 +123,11 @@ static __global__ void __launch_bounds__(kThreads) hs_gather_update_kernel(const
     const int pat = blockIdx.x, np = a.f.np;
     if (threadIdx.x == 0) {
         int ok = 1;
+        const unsigned long long epoch = *a.epoch0 + (unsigned long long)a.pass + 1ull;
         const unsigned long long t0 = hs_globaltimer();
         for (int r = 0; r < a.world && ok; ++r) {
             unsigned long long v;
-            while (((v = hs_ld_acquire_sys(a.flags_local + r)) & ~kXchgAbort) < a.epoch) {
+            while (((v = hs_ld_acquire_sys(a.flags_local + r)) & ~kXchgAbort) < epoch) {
                 __nanosleep(128);
                 if (hs_globaltimer() - t0 > kXchgTimeoutNs) {  // a peer never published
                     ok = 0;

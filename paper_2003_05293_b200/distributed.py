@@ -125,8 +125,7 @@ def solve_sharded(pupil, spots, config, rank: int, world: int, all_gather, devic
         handles = all_gather(plan.p2p_setup())
         try:
             plan.p2p_open(handles)
-            for j in range(passes):
-                plan.p2p_pass(j)
+            plan.p2p_solve()  # all passes as one captured graph (hs_shard_p2p_solve)
             plan.sync()
         finally:
             all_gather(None)  # every rank finished reading its peers' buffers

@@ -1,2 +1,2 @@
-rm -f gpurun_out/cpc.txt
-for c in 0 1 2 4 8 16; do echo "cpc $c" >> gpurun_out/cpc.txt; HS_SLAB_CPC=$c timeout 300 python tools/ab_time.py >> gpurun_out/cpc.txt 2>&1; done
+timeout 900 python -m pytest tests/test_gpu_sharded.py -q > gpurun_out/sharded.txt 2>&1
+timeout 400 python bench.py --gpus 2 --workload cfg4 --steps 10 --no-cpu > gpurun_out/bench_g2_cfg4.json 2> gpurun_out/bench_g2_cfg4.err
