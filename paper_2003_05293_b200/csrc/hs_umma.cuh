@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     const int xb_c = tid & (kUC - 1), xb_kq = (tid >> 6) & 1;
     const float4 *xb_src = reinterpret_cast<const float4 *>(gx + (int64_t)min(c0 + xb_c, a.side - 1) * a.np);
     constexpr int XV = kUQ / 2;  // float4 (two complex) per thread and k-step
-    float4 xq[XV], xn[XV];       // k-step ks, ks + 1
+    float4 xn[XV];               // gx of the next k-step to build
     auto load_b = [&](int ks, float4 (&d)[XV]) {
         if (xb_on && ks < ksteps) {
             const int k = ks * kUF + kUQ * xb_kq;
@@ -420,8 +420,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
             for (int i = 0; i < XV; ++i) d[i] = __ldg(xb_src + k / 2 + i);
         }
     };
-    load_b(0, xq);  // gx: an input of the whole solve
-    load_b(1, xn);
+    load_b(0, xn);  // gx: an input of the whole solve
 
     // -- below: the previous pass's results (status, coef); TMEM is taken
     // only now, so a dependent-launched CTA never holds it while waiting
@@ -571,6 +570,28 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
         }
         ++folded;
     };
+    // The producers build step ks + 1's X' chunks (registers) right after
+    // publishing step ks, so after the wait for a free slot only the stores
+    // remain on the MMA's critical path.
+    uint4 pre[4];  // X'(step) chunks: re hi, re lo, im hi, im lo
+    auto make_x = [&](int ks) {  // X' = coef_k gx[c][k]: kUQ spots of column c
+        const int k = ks * kUF + kUQ * xb_kq;
+        float xr[kUQ], xi[kUQ];
+#pragma unroll
+        for (int i = 0; i < kUQ; ++i) {
+            const float2 w = coef_s[k + i];
+            const float4 u = xn[i / 2];
+            const float ur = (i & 1) ? u.z : u.x, ui = (i & 1) ? u.w : u.y;
+            xr[i] = fmaf(w.x, ur, -w.y * ui);
+            xi[i] = fmaf(w.x, ui, w.y * ur);
+        }
+        hs_split_chunk(xr, pre[0], pre[1]);
+        hs_split_chunk(xi, pre[2], pre[3]);
+    };
+    if (xb_on && ksteps > 0) {
+        make_x(0);
+        load_b(1, xn);
+    }
     for (int ks = 0; ks < ksteps; ++ks) {
         if (ks >= 2) wait_mma(ks - 2);  // A slot of ks + 1, B slot of ks free
         if (ks < 16) TR(kUThreads - 2 * kUC, 64 + ks);
@@ -579,39 +600,26 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
             while (folded < (ks - 1) / KG) fold_group();
         if (tid == 0) tma_ahead(ks);
         if (ks < 16) TR(0, 48 + ks);
-        if (xb_on) {  // X' = coef_k gx[c][k]: kUQ spots of column c, one 16-byte chunk per plane
-            const int k = ks * kUF + kUQ * xb_kq;
-            float xr[kUQ], xi[kUQ];
-#pragma unroll
-            for (int i = 0; i < kUQ; ++i) {
-                const float2 w = coef_s[k + i];
-                const float4 u = xq[i / 2];
-                const float ur = (i & 1) ? u.z : u.x, ui = (i & 1) ? u.w : u.y;
-                xr[i] = fmaf(w.x, ur, -w.y * ui);
-                xi[i] = fmaf(w.x, ui, w.y * ur);
-            }
-            uint4 rh, rl, ih, il;
-            hs_split_chunk(xr, rh, rl);
-            hs_split_chunk(xi, ih, il);
+        if (xb_on) {  // step ks's X' chunks (built ahead), one 16-byte chunk per plane
             // planes [128 rows][kUF spots] (hs_uoffb): B1 = [Xr; Xi], B2 = [-Xi; Xr]
             unsigned char *d = sbase + kUA * kUASlot + (ks % kUB) * kUBSlot + xb_c * 16 + xb_kq * 2048;
             constexpr int R64 = kUC * 16;  // row 64
-            const uint4 nih = hs_neg_chunk(ih), nil = hs_neg_chunk(il);
-            *reinterpret_cast<uint4 *>(d) = rh;
-            *reinterpret_cast<uint4 *>(d + R64) = ih;
-            *reinterpret_cast<uint4 *>(d + kUAPl) = rl;
-            *reinterpret_cast<uint4 *>(d + kUAPl + R64) = il;
-            *reinterpret_cast<uint4 *>(d + 2 * kUAPl) = nih;
-            *reinterpret_cast<uint4 *>(d + 2 * kUAPl + R64) = rh;
-            *reinterpret_cast<uint4 *>(d + 3 * kUAPl) = nil;
-            *reinterpret_cast<uint4 *>(d + 3 * kUAPl + R64) = rl;
+            *reinterpret_cast<uint4 *>(d) = pre[0];
+            *reinterpret_cast<uint4 *>(d + R64) = pre[2];
+            *reinterpret_cast<uint4 *>(d + kUAPl) = pre[1];
+            *reinterpret_cast<uint4 *>(d + kUAPl + R64) = pre[3];
+            *reinterpret_cast<uint4 *>(d + 2 * kUAPl) = hs_neg_chunk(pre[2]);
+            *reinterpret_cast<uint4 *>(d + 2 * kUAPl + R64) = pre[0];
+            *reinterpret_cast<uint4 *>(d + 3 * kUAPl) = hs_neg_chunk(pre[3]);
+            *reinterpret_cast<uint4 *>(d + 3 * kUAPl + R64) = pre[1];
         }
-#pragma unroll
-        for (int i = 0; i < XV; ++i) xq[i] = xn[i];
-        load_b(ks + 2, xn);  // two k-steps in flight
         if (ks < 16) TR(kUThreads - 2 * kUC, 80 + ks);
 
         publish(ks);
+        if (xb_on && ks + 1 < ksteps) {
+            make_x(ks + 1);
+            load_b(ks + 2, xn);
+        }
         if (tid == 0) {
             wait_tma(ks);  // gy planes landed
             if (ks < 16) TR(0, 112 + ks);
