@@ -201,6 +201,35 @@ def cpu_oracle_rate(seconds=10.0, threads=None):
     return done / el, done, threads
 
 
+def _pool_worker(job):
+    """One process of the process-pool CPU leg: single-threaded oracle solves
+    (+ e/u) of the workload until the deadline."""
+    seconds, first = job
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    import paper_2003_05293_b200 as hs
+    pupil = hs.build_pupil(SIDE)
+    done, eu, t0 = 0, [], time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        k = first + done
+        s = hs.random_foci(NSPOTS, 1000 + k)
+        r = oracle.solve(pupil, s.x, s.y, s.z, s.amplitude, "cswgs", ITERS, COMPRESSION, seed=k, threads=1)
+        eu.append(oracle.quality(pupil, r["tables"], r["phase"], s.amplitude, threads=1)[:2])
+        done += 1
+    return done, time.perf_counter() - t0, eu
+
+
+def cpu_pool_rate(seconds, procs):
+    """Holograms/s of `procs` single-threaded oracle processes (the reference
+    bench's ProcessPoolExecutor variant, which beat its threads: SURVEY 8(d))."""
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+    with ProcessPoolExecutor(procs, mp_context=mp.get_context("spawn")) as ex:
+        res = list(ex.map(_pool_worker, [(seconds, 100000 * (i + 1)) for i in range(procs)]))
+    rate = sum(d / el for d, el, _ in res)
+    return rate, sum(d for d, _, _ in res), [x for _, _, e in res for x in e]
+
+
 def run_reference(args):
     rank, _, world = dist_env()
     if rank != 0:
@@ -222,7 +251,14 @@ def run_reference(args):
     t0 = time.perf_counter()
     eu = [step(args.warmup + k)[:2] for k in range(args.steps)]
     el = time.perf_counter() - t0
-    val = args.steps / el
+    thread_rate = args.steps / el
+    # the process-pool variant (one single-threaded solver per core), run for
+    # as long as the threaded leg; the better of the two is the reference rate
+    pool_rate, pool_done, pool_eu = cpu_pool_rate(min(max(el, 5.0), 60.0), threads)
+    val = max(thread_rate, pool_rate)
+    variant = "process pool" if pool_rate > thread_rate else "threads"
+    if pool_rate > thread_rate:
+        eu = pool_eu
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "holograms/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -232,9 +268,13 @@ def run_reference(args):
                                "sample; holograms are independent, so the rate is per hologram)",
             "cpu_baseline": {"value": val, "unit": "holograms/s", "cores": threads,
                              "kind": "port", "cpu_model": cpu_model(),
-                             "threading": "OpenMP (libgomp), the reference's prange units",
-                             "sample": f"{args.steps} holograms of the "
-                             "workload, 1 per step (C+OpenMP oracle, bit-exact vs reference)"},
+                             "threading": f"{variant} (the better of: OpenMP threads over the "
+                                          "reference's prange units, "
+                                          f"{thread_rate:.3f} holo/s; {threads} single-threaded "
+                                          f"processes, {pool_rate:.3f} holo/s)",
+                             "sample": f"{args.steps} holograms of the workload, 1 per step, "
+                             f"threaded; {pool_done} holograms in the process pool "
+                             "(C+OpenMP oracle, bit-exact vs reference)"},
             "e2e": {"value": val, "unit": "holograms/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "mean_e": float(np.mean([e for e, _ in eu])),
@@ -435,9 +475,15 @@ def run_ours(args):
     if world == 1 and not args.no_cpu:
         rate, done, threads = cpu_oracle_rate(args.cpu_seconds)
         rate1, done1, _ = cpu_oracle_rate(max(2.0, args.cpu_seconds / 2), threads=1)
-        cpu = {"value": rate, "unit": "holograms/s", "cores": threads, "kind": "port",
-               "cpu_model": cpu_model(), "threading": "OpenMP (libgomp), the reference's "
-               "prange units (pixels for the backward pass, 1024-pixel chunks forward)",
+        prate, pdone, _ = cpu_pool_rate(args.cpu_seconds, threads)
+        cpu = {"value": max(rate, prate), "unit": "holograms/s", "cores": threads, "kind": "port",
+               "cpu_model": cpu_model(), "threading": "the better of OpenMP (libgomp) threads over the "
+               "reference's prange units (pixels for the backward pass, 1024-pixel chunks forward) "
+               "and a process pool of single-threaded solvers (SURVEY 8(d), config 5)",
+               "threads": {"value": rate, "unit": "holograms/s", "cores": threads,
+                           "sample": f"{done} holograms"},
+               "process_pool": {"value": prate, "unit": "holograms/s", "processes": threads,
+                                "sample": f"{pdone} holograms"},
                "workers_1": {"value": rate1, "unit": "holograms/s", "cores": 1,
                              "sample": f"{done1} holograms"},
                "sample": f"{done} holograms of the workload (CS-WGS 1152^2 N=100 I=20 + e/u), "
