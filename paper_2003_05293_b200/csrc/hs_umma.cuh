@@ -654,9 +654,19 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
         while (folded < (ksteps + KG - 1) / KG) fold_group();
 
     // ---- S -> b = A conj(S)/|S| (registers), phase write --------------------
+    // S of 8 pixels per step, double-buffered: the next step's TMEM loads are
+    // issued right after the wait for the current one's
+    float sbuf[2][16];  // [buffer][Sr 8 | Si 8]
+    auto ld_s = [&](int cc, float *d) {
+        hs_tc_ld4(tl + cc * 8 + 4 * h, d);
+        hs_tc_ld4(tl + (cc + 1) * 8 + 4 * h, d + 4);
+        hs_tc_ld4(tl + kUC + cc * 8 + 4 * h, d + 8);
+        hs_tc_ld4(tl + kUC + (cc + 1) * 8 + 4 * h, d + 12);
+    };
+    if (!CH) ld_s(0, sbuf[0]);
 #pragma unroll
     for (int cc = 0; cc < NG8; cc += 2) {
-        float sr[8], si[8];
+        float *sr = sbuf[(cc >> 1) & 1], *si = sr + 8;
         if (CH) {
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
@@ -664,11 +674,8 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
                 si[jj] = sacc[32 + 4 * cc + jj];
             }
         } else {
-            hs_tc_ld4(tl + cc * 8 + 4 * h, sr);
-            hs_tc_ld4(tl + (cc + 1) * 8 + 4 * h, sr + 4);
-            hs_tc_ld4(tl + kUC + cc * 8 + 4 * h, si);
-            hs_tc_ld4(tl + kUC + (cc + 1) * 8 + 4 * h, si + 4);
             hs_tc_wait_ld();
+            if (cc + 2 < NG8) ld_s(cc + 2, sbuf[((cc >> 1) + 1) & 1]);
         }
         int dix[8];  // storage indices of the 8 pixels (WRITE), two aligned int4 when side % 4 == 0
         if (WRITE) {
