@@ -825,13 +825,18 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        float tq[2][16];  // T of the group's two 8-spot halves: [e][Tr 8 | Ti 8], one wait for both
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+            if (8 * e < KQ) {
+                hs_tc_ld8(tl + kk + 8 * e, *reinterpret_cast<float (*)[8]>(tq[e]));
+                hs_tc_ld8(tl + NP + kk + 8 * e, *reinterpret_cast<float (*)[8]>(tq[e] + 8));
+            }
+        hs_tc_wait_ld();
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             if (8 * e < KQ) {
-                float tr[8], ti[8];
-                hs_tc_ld8(tl + kk + 8 * e, tr);
-                hs_tc_ld8(tl + NP + kk + 8 * e, ti);
-                hs_tc_wait_ld();
+                const float *tr = tq[e], *ti = tq[e] + 8;
                 const float gr[8] = {gc[e][0].x, gc[e][0].y, gc[e][0].z, gc[e][0].w,
                                      gc[e][2].x, gc[e][2].y, gc[e][2].z, gc[e][2].w};
                 const float gi[8] = {gc[e][1].x, gc[e][1].y, gc[e][1].z, gc[e][1].w,
