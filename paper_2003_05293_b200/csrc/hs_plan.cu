@@ -528,6 +528,9 @@ void free_graphs(hs_plan *p)
 {
     for (auto &kv : p->graphs) cudaGraphExecDestroy(kv.second);
     p->graphs.clear();
+    // captured sharded solves hold the same buffers (tables, lists, partials)
+    for (auto &kv : p->xchg.graphs) cudaGraphExecDestroy(kv.second);
+    p->xchg.graphs.clear();
 }
 
 void free_fold(hs_plan *p)
