@@ -560,6 +560,7 @@ void free_batch(hs_plan *p)
         p->slot32[k] = false;
     }
     dfree(p->d_raster);
+    dfree(p->d_trace);
     dfree(p->d_phase);
     p->d_out[0] = nullptr;
     dfree(p->d_trace_w); dfree(p->d_trace_m);
@@ -872,6 +873,10 @@ int launch_slab(hs_plan *p, int mode, const DevList &l, int32_t nunits, const Up
     a.gy = p->d_gy + p->view0 * a.tab_stride;
     a.coef = p->d_coef + (int64_t)p->view0 * c.np;
     a.f = fold_args(p, nunits, u, lo, hi);
+    if (p->trace_next) {
+        a.trace = p->d_trace;
+        p->trace_next = false;
+    }
     const int64_t span = (hi - lo) / 2;  // chunks
     const bool half = span * p->batch * 4 < (int64_t)p->num_sms * 3;
     int best = 1;
@@ -2374,8 +2379,21 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
     CUDA_TRY(cudaEventCreate(&e0));
     CUDA_TRY(cudaEventCreate(&e1));
     const UpdArgs u = upd_args(p, ACT_FIELDS);
+    if (which == 1 && getenv("HS_SLAB_TRACE")) {  // timing probe of one window-pass CTA
+        if (!p->d_trace && (rc = dalloc(&p->d_trace, 128))) return rc;
+        CUDA_TRY(cudaMemset(p->d_trace, 0, 128 * sizeof(unsigned long long)));
+        p->trace_next = true;
+        if ((rc = launch_pass(p, PM_BWD | PM_FWD, *l, 0, l->count, 0, nullptr, nullptr, 0, u))) return rc;
+        CUDA_TRY(cudaStreamSynchronize(p->stream));
+        unsigned long long t[128];
+        CUDA_TRY(cudaMemcpy(t, p->d_trace, sizeof t, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "slab trace (cycles from CTA start):");
+        for (int i = 1; i < 128; ++i)
+            if (t[i]) fprintf(stderr, " %d:%lld", i, (long long)(t[i] - t[0]));
+        fprintf(stderr, "\n");
+    }
     if (which == 0 && getenv("HS_UMMA_TRACE")) {  // timing probe of one tcgen05 CTA
-        if ((rc = dalloc(&p->d_trace, 128))) return rc;
+        if (!p->d_trace && (rc = dalloc(&p->d_trace, 128))) return rc;
         CUDA_TRY(cudaMemset(p->d_trace, 0, 128 * sizeof(unsigned long long)));
         p->trace_next = true;
         if ((rc = launch_tile(p, false, u, nullptr))) return rc;

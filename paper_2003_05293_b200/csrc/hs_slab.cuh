@@ -66,6 +66,7 @@ struct SlabArgs {
     const float2 *gx, *gy;    // [B][side][np]
     const float2 *coef;       // [B][np]
     FoldArgs f;
+    unsigned long long *trace;  // timing probe of one CTA (HS_SLAB_TRACE), normally null
 };
 
 __host__ __device__ constexpr size_t hs_slab_fixed_bytes(int np)
@@ -157,6 +158,11 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
     __shared__ int s_next_c0;
 
     hs_pdl_launch_next();
+    const bool trc = a.trace && blockIdx.x == (gridDim.x > 20 ? 20u : gridDim.x / 2) && blockIdx.y == 0;
+    auto TR = [&](int slot) {
+        if (trc && threadIdx.x == 0) a.trace[slot] = clock64();
+    };
+    TR(0);
     const int pat = blockIdx.y;
     // fold units are half-chunks (16 streams); a whole-chunk CTA streams cpc
     // chunks, a half-chunk CTA (small batches: twice the CTAs) one half
@@ -537,7 +543,9 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
         }
     };
 
+    TR(1);
     for (int qi = 0; qi < nq; ++qi) {
+        if (qi < 16) TR(2 + 3 * qi);
         fetch_ent(qi + 2);
         // the next chunk's slab origin, read now (the previous chunk's last
         // barrier ordered the previous reads of s_next_c0 before this write)
@@ -551,12 +559,16 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
                 for (int u = 0; u < 16; u += 2) pair(qi, t + u);
             }
         }
+        if (qi < 16) TR(3 + 3 * qi);
         chunk_end(qi);
+        if (qi < 16) TR(4 + 3 * qi);
     }
+    TR(60);
     if (a.f.u.act != ACT_NONE) {
         __syncthreads();
         hs_fold(a.f, pat, 2 * q0 + half, reinterpret_cast<char *>(Es), HALF ? 1 : 2 * nq);
     }
+    TR(61);
 }
 
 typedef void (*SlabFn)(SlabArgs);

@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_sharded.py -q > gpurun_out/sharded.txt 2>&1
-timeout 400 python bench.py --gpus 2 --workload cfg4 --steps 10 --no-cpu > gpurun_out/bench_g2_cfg4.json 2> gpurun_out/bench_g2_cfg4.err
+HS_SLAB_TRACE=1 timeout 300 python tools/profile_pass.py --which 1 --batch 32 > gpurun_out/strace.txt 2>&1
+HS_SLAB_TRACE=1 timeout 300 python tools/profile_pass.py --which 1 --batch 16 >> gpurun_out/strace.txt 2>&1
+HS_SLAB_TRACE=1 timeout 300 python tools/profile_pass.py --which 1 --batch 1 >> gpurun_out/strace.txt 2>&1
