@@ -434,14 +434,23 @@ __device__ __forceinline__ void hs_fold(const FoldArgs &a, int pat, int chunk, c
     if (!s_last) return;
     __threadfence();
     double2 *gp = a.gpart + (int64_t)pat * a.gpart_stride;
+    // Loads are issued 8 at a time ahead of the (chunk-ordered) sums: a few L2
+    // round trips on the fold tail instead of c1 - c0 dependent ones.
     if (a.partials64) {
         const double2 *part = a.partials64 + (int64_t)pat * a.part_stride;
         for (int k = tid; k < np; k += kThreads) {
             double sx = 0.0, sy = 0.0;
-            for (int c = c0; c < c1; ++c) {
-                const double2 v = __ldcg(part + (int64_t)c * np + k);
-                sx += v.x;
-                sy += v.y;
+            for (int cb = c0; cb < c1; cb += 8) {
+                double2 v[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (cb + c < c1) v[c] = __ldcg(part + (int64_t)(cb + c) * np + k);
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (cb + c < c1) {
+                        sx += v[c].x;
+                        sy += v[c].y;
+                    }
             }
             gp[(int64_t)grp * np + k] = make_double2(sx, sy);
         }
@@ -449,10 +458,17 @@ __device__ __forceinline__ void hs_fold(const FoldArgs &a, int pat, int chunk, c
         const float2 *part = a.partials + (int64_t)pat * a.part_stride;
         for (int k = tid; k < np; k += kThreads) {
             double sx = 0.0, sy = 0.0;
-            for (int c = c0; c < c1; ++c) {
-                const float2 v = __ldcg(part + (int64_t)c * np + k);
-                sx += (double)v.x;
-                sy += (double)v.y;
+            for (int cb = c0; cb < c1; cb += 8) {
+                float2 v[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (cb + c < c1) v[c] = __ldcg(part + (int64_t)(cb + c) * np + k);
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (cb + c < c1) {
+                        sx += (double)v[c].x;
+                        sy += (double)v[c].y;
+                    }
             }
             gp[(int64_t)grp * np + k] = make_double2(sx, sy);
         }
@@ -472,10 +488,17 @@ __device__ __forceinline__ void hs_fold(const FoldArgs &a, int pat, int chunk, c
     double *mag_s = reinterpret_cast<double *>(E + np);           // [2*np]
     for (int k = tid; k < np; k += kThreads) {
         double sx = 0.0, sy = 0.0;
-        for (int gI = 0; gI < ngroups; ++gI) {
-            const double2 v = __ldcg(gp + (int64_t)gI * np + k);
-            sx += v.x;
-            sy += v.y;
+        for (int g0 = 0; g0 < ngroups; g0 += 8) {  // 8 loads in flight, summed in group order
+            double2 v[8];
+#pragma unroll
+            for (int gI = 0; gI < 8; ++gI)
+                if (g0 + gI < ngroups) v[gI] = __ldcg(gp + (int64_t)(g0 + gI) * np + k);
+#pragma unroll
+            for (int gI = 0; gI < 8; ++gI)
+                if (g0 + gI < ngroups) {
+                    sx += v[gI].x;
+                    sy += v[gI].y;
+                }
         }
         E[k] = make_double2(sx, sy);
     }

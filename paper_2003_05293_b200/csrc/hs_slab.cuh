@@ -336,8 +336,12 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
     stage(__ldg(a.chunk_c0 + q0));  // gx (tables) and lists: inputs of the whole solve
     // -- everything below reads the previous pass's results (status, coef)
     hs_pdl_wait_prev();
+    // coefficient and status loads in flight together (one L2 round trip on
+    // the pass's critical path, which is what a single hologram waits on)
+    static_assert(NP <= NT, "one coefficient per thread");
+    const float2 cfv = tid < NP ? a.coef[(int64_t)pat * NP + tid] : make_float2(0.f, 0.f);
     if (a.f.u.status[pat] != 0) return;  // uniform per CTA
-    for (int k = tid; k < NP; k += NT) coef_s[k] = a.coef[(int64_t)pat * NP + k];
+    if (tid < NP) coef_s[tid] = cfv;
     __syncthreads();
     int rcur = -1;
     // smem address of this stream's entries in chunk buffer 0 / 1
