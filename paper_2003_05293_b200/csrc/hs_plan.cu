@@ -744,9 +744,7 @@ int launch_tables(hs_plan *p, bool seed, bool with_prep = true)
                                                   seed ? p->d_theta : nullptr, p->d_coef, p->d_w);
     CUDA_TRY(cudaGetLastError());
     if (with_prep && p->d_gyp && tile_set(p).umma) {
-        dim3 pg((unsigned)((p->side + kUR - 1) / kUR * (p->cfg.np / kUF) +
-                           hs_umma_xblocks(p->side) * hs_umma_nsc(p->cfg.np)),
-                p->batch);
+        dim3 pg((unsigned)hs_umma_prep_blocks(p->side, p->cfg.np), p->batch);
         hs_umma_prep_kernel<<<pg, 256, 0, p->stream>>>(p->d_gx, p->d_gy, p->d_gyp, p->side, p->cfg.np,
                                                        (int64_t)p->side * p->cfg.np, p->gyp_stride);
         CUDA_TRY(cudaGetLastError());
@@ -1114,9 +1112,7 @@ int record_solve(hs_plan *p, int alg, int iters, int64_t subset, int flags, doub
     if (!p->use64 && p->d_gyp && tile_set(p).umma) {
         CUDA_TRY(cudaEventRecord(p->fork_ev, p->stream));
         CUDA_TRY(cudaStreamWaitEvent(p->stream3, p->fork_ev, 0));
-        dim3 pg((unsigned)((p->side + kUR - 1) / kUR * (p->cfg.np / kUF) +
-                           hs_umma_xblocks(p->side) * hs_umma_nsc(p->cfg.np)),
-                p->batch);
+        dim3 pg((unsigned)hs_umma_prep_blocks(p->side, p->cfg.np), p->batch);
         hs_umma_prep_kernel<<<pg, 256, 0, p->stream3>>>(p->d_gx, p->d_gy, p->d_gyp, p->side, p->cfg.np,
                                                         (int64_t)p->side * p->cfg.np, p->gyp_stride);
         CUDA_TRY(cudaGetLastError());

@@ -35,7 +35,7 @@
 // step ahead; the per-pass coefficients go on the B side of the backward
 // (X' = coef_k gx[c][k], built by warps 4-7) and b' (A of the forward) is
 // written by every thread for its row.  The gy planes also give the E
-// epilogue coalesced gy reads (hi + lo == gy to 2^-22).  Shared memory: A and
+// epilogue reads gy in fp32 from a row-coalesced copy written beside them.  Shared memory: A and
 // B rings of 3 x 16 KB, SWIZZLE_NONE K-major canonical layout (8 x 16-byte
 // core matrices).  Per k-step every thread arrives on an operand mbarrier
 // after writing its part (no CTA-wide barrier); thread 0 waits for it and
@@ -131,9 +131,23 @@ __host__ __device__ constexpr int64_t hs_umma_xblock_floats(int np)
 {
     return (int64_t)hs_umma_nsc(np) * 4 * hs_umma_npc(np) * 8;  // 4 planes x npc rows x 32 bytes
 }
+// gy in fp32 for the E epilogue: [band][8-spot block][4][128 rows] float4
+// (re of spots 0-3, im 0-3, re 4-7, im 4-7): a thread (row) reads 4
+// coalesced float4 per 8 spots, no operand-format decode
+__host__ __device__ constexpr int64_t hs_umma_gye_floats(int side, int np)
+{
+    return (int64_t)((side + kUR - 1) / kUR) * np * 4 * kUR / 2;
+}
 __host__ __device__ constexpr int64_t hs_umma_plane_floats(int side, int np)
 {
-    return hs_umma_gy_floats(side, np) + (int64_t)hs_umma_xblocks(side) * hs_umma_xblock_floats(np);
+    return hs_umma_gy_floats(side, np) + (int64_t)hs_umma_xblocks(side) * hs_umma_xblock_floats(np) +
+           hs_umma_gye_floats(side, np);
+}
+// grid.x of hs_umma_prep_kernel
+__host__ __device__ constexpr int hs_umma_prep_blocks(int side, int np)
+{
+    return (side + kUR - 1) / kUR * (np / kUF) + hs_umma_xblocks(side) * hs_umma_nsc(np) +
+           (side + kUR - 1) / kUR * (np / 8);
 }
 
 // Byte offset of element (r, k) in a [128 rows][kUF] K-major operand plane
@@ -216,6 +230,24 @@ static __global__ void hs_umma_prep_kernel(const float2 *__restrict__ gx, const 
             const int o = hs_uoffb(r, k);
             hs_split_store(v.x, dst + o, kUAPl);
             hs_split_store(v.y, dst + o + 2 * kUAPl, kUAPl);
+        }
+    } else if ((int)blockIdx.x >= ngy + hs_umma_xblocks(side) * hs_umma_nsc(np)) {
+        const int e = blockIdx.x - ngy - hs_umma_xblocks(side) * hs_umma_nsc(np);  // band * np / 8 + block
+        const int band = e / (np / 8), blk = e % (np / 8);
+        float4 *dst = reinterpret_cast<float4 *>(planes + (int64_t)pat * plane_stride + hs_umma_gy_floats(side, np) +
+                                                 (int64_t)hs_umma_xblocks(side) * hs_umma_xblock_floats(np)) +
+                      (int64_t)e * 4 * kUR;
+        for (int i = threadIdx.x; i < 4 * kUR; i += blockDim.x) {
+            const int qd = i / kUR, r = i % kUR;  // quad qd: spots 4 (qd / 2) .., re (qd even) / im
+            const int grow = band * kUR + r;
+            float v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 g = grow < side ? gy[(int64_t)pat * tab_stride + (int64_t)grow * np + blk * 8 + 4 * (qd >> 1) + j]
+                                             : make_float2(0.f, 0.f);
+                v[j] = (qd & 1) ? g.y : g.x;
+            }
+            dst[qd * kUR + r] = make_float4(v[0], v[1], v[2], v[3]);
         }
     } else {
         const int nsc = hs_umma_nsc(np), npc = hs_umma_npc(np);
@@ -768,50 +800,26 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     // ---- E_k = sum_r gy[r][k] T[r][k]: spots KH h .. KH (h+1) of the row, 16
     // at a time; each group of 16 (32 values) is transpose-reduced over the
     // warp's 32 rows (one value per lane), then the 4 lane-quarter warps are
-    // summed in order through shared memory.  gy comes from the planes
-    // (hi + lo == gy to 2^-22), coalesced over the rows; the next group's planes are
+    // summed in order through shared memory.  gy comes from its fp32 copy in
+    // the row-coalesced E layout (hs_umma_gye_floats); the next group's gy is
     // loaded while the current one is reduced.
     const int k0 = sc * NP;             // first spot of the chunk
     constexpr int NG = (KH + 15) / 16;  // groups of 16 spots (the last may hold 8)
     float4 gq[2][2][4];                 // [buffer][quad-pair half][plane]
+    // fp32 gy of this band (hs_umma_gye_floats layout), row-coalesced
+    const float4 *gye = reinterpret_cast<const float4 *>(pbase + hs_umma_gy_floats(a.side, a.np) +
+                                                         (int64_t)hs_umma_xblocks(a.side) * hs_umma_xblock_floats(a.np) +
+                                                         (int64_t)(r0 / kUR) * a.np * 4 * kUR / 2) + row;
     auto load_g = [&](int g, float4 (&d)[2][4]) {
         const int kk = KH * h + 16 * g;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {  // k8 block e of the group
             if (16 * g + 8 * e < KH) {
-                // spots past np (last chunk's padding): any finite plane data, T is 0 there
+                // spots past np (last chunk's padding): any finite data, T is 0 there
                 const int sp = min(k0 + kk + 8 * e, a.np - 8);  // first of 8 spots (multiple of 8)
-                const int blk = sp / kUF;
-                if constexpr (kF16) {
-                    // the 8 spots are one K half of the block: one 16-byte chunk per plane
-                    const unsigned char *pb = reinterpret_cast<const unsigned char *>(gyp) +
-                                              (int64_t)blk * kUASlot + ((sp % kUF) / 8) * 2048 + row * 16;
-                    uint4 c[4];
+                const float4 *pe = gye + (int64_t)(sp / 8) * 4 * kUR;
 #pragma unroll
-                    for (int pl = 0; pl < 4; ++pl) c[pl] = __ldg(reinterpret_cast<const uint4 *>(pb + pl * kUAPl));
-                    auto h2 = [](uint32_t w, int hi) { return hs_opnd(hi ? w >> 16 : w & 0xffffu); };
-#pragma unroll
-                    for (int hq = 0; hq < 2; ++hq) {  // spots 4 hq .. 4 hq + 3 -> d[e][2 hq] (re), d[e][2 hq + 1] (im)
-                        const uint32_t r0w = hq ? c[0].z : c[0].x, r1w = hq ? c[0].w : c[0].y;
-                        const uint32_t l0w = hq ? c[1].z : c[1].x, l1w = hq ? c[1].w : c[1].y;
-                        const uint32_t i0w = hq ? c[2].z : c[2].x, i1w = hq ? c[2].w : c[2].y;
-                        const uint32_t m0w = hq ? c[3].z : c[3].x, m1w = hq ? c[3].w : c[3].y;
-                        d[e][2 * hq] = make_float4(h2(r0w, 0) + h2(l0w, 0), h2(r0w, 1) + h2(l0w, 1),
-                                                   h2(r1w, 0) + h2(l1w, 0), h2(r1w, 1) + h2(l1w, 1));
-                        d[e][2 * hq + 1] = make_float4(h2(i0w, 0) + h2(m0w, 0), h2(i0w, 1) + h2(m0w, 1),
-                                                       h2(i1w, 0) + h2(m1w, 0), h2(i1w, 1) + h2(m1w, 1));
-                    }
-                } else {
-                    const float4 *pb = reinterpret_cast<const float4 *>(gyp + (int64_t)blk * (kUASlot / 4)) + row;
-#pragma unroll
-                    for (int hq = 0; hq < 2; ++hq) {
-                        // quad hq of block e -> d[e][2 hq] (re: hi + lo), d[e][2 hq + 1] (im)
-                        const float4 rh = __ldg(pb + hq * 128), rl = __ldg(pb + 256 + hq * 128);
-                        const float4 ih = __ldg(pb + 512 + hq * 128), il = __ldg(pb + 768 + hq * 128);
-                        d[e][2 * hq] = make_float4(rh.x + rl.x, rh.y + rl.y, rh.z + rl.z, rh.w + rl.w);
-                        d[e][2 * hq + 1] = make_float4(ih.x + il.x, ih.y + il.y, ih.z + il.z, ih.w + il.w);
-                    }
-                }
+                for (int qd = 0; qd < 4; ++qd) d[e][qd] = __ldg(pe + qd * kUR);
             }
         }
     };
