@@ -355,13 +355,25 @@ __device__ __forceinline__ void hs_update(const UpdArgs &a, int b, double2 *E, d
     }
     // ACT_STEP: rebalance_weights (solvers.py:104-129), then the coefficient
     // update a = w a0, theta = arg E (solvers.py:148-151, kernels.py:206-208).
+    // theta and its sincos depend on E alone: they are computed in the first
+    // loop (E[k] is replaced by (cos, sin)), off the chain of reductions.
     int zeros = 0;
-    double minpos = INFINITY;
+    double minpos = INFINITY, msum = 0.0;
     for (int k = tid; k < n; k += kThreads) {
-        const double m = hypot(E[k].x, E[k].y);
+        const double er = E[k].x, ei = E[k].y;
+        const double m = hypot(er, ei);
         mag_s[k] = m;
         if (m == 0.0) ++zeros;
         else minpos = fmin(minpos, m);
+        msum += m;
+        double th = 0.0;                                   // solvers.py:96-101
+        if (er != 0.0 || ei != 0.0) {
+            th = atan2(ei, er);
+            if (th == kPi) th = -kPi;
+        }
+        double sn, co;
+        sincos(th, &sn, &co);
+        E[k] = make_double2(co, sn);
     }
     zeros = hs_tree(ibuf, zeros, ISum());
     if (zeros > 0) {
@@ -370,12 +382,13 @@ __device__ __forceinline__ void hs_update(const UpdArgs &a, int b, double2 *E, d
             if (tid == 0) a.status[b] = 3;  // HS_EDEGENERATE
             return;
         }
-        for (int k = tid; k < n; k += kThreads)
+        msum = 0.0;
+        for (int k = tid; k < n; k += kThreads) {
             if (mag_s[k] == 0.0) mag_s[k] = minpos * 1e-6;  // DEGENERACY_FLOOR
+            msum += mag_s[k];
+        }
         if (tid == 0 && a.degen[b] == 0) a.degen[b] = a.iter + 1;
     }
-    double msum = 0.0;
-    for (int k = tid; k < n; k += kThreads) msum += mag_s[k];
     msum = hs_tree(dbuf, msum, DSum());
     const double mean = msum / (double)n;
     int bad = 0;
@@ -396,16 +409,9 @@ __device__ __forceinline__ void hs_update(const UpdArgs &a, int b, double2 *E, d
         a.trace_m[tix] = mag_s[k];
         a.w[(int64_t)b * np + k] = wk;
         const double am = wk * a.a0[(int64_t)b * n + k];
-        const double er = E[k].x, ei = E[k].y;
-        double th = 0.0;                                   // solvers.py:96-101
-        if (er != 0.0 || ei != 0.0) {
-            th = atan2(ei, er);
-            if (th == kPi) th = -kPi;
-        }
-        double s, co;
-        sincos(th, &s, &co);
-        if (a.coef64) a.coef64[(int64_t)b * np + k] = make_double2(am * co, am * s);
-        else a.coef[(int64_t)b * np + k] = make_float2((float)(am * co), (float)(am * s));
+        const double co = E[k].x, sn = E[k].y;
+        if (a.coef64) a.coef64[(int64_t)b * np + k] = make_double2(am * co, am * sn);
+        else a.coef[(int64_t)b * np + k] = make_float2((float)(am * co), (float)(am * sn));
     }
 }
 
