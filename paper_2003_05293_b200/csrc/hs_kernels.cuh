@@ -41,6 +41,7 @@ constexpr int kThreads = 256;        // pass-kernel CTA size (8 warps)
 constexpr int kWarps = kThreads / 32;
 constexpr int kTargetChunks = 296;   // sparse lists: chunks per pattern (2 x 148 SMs)
 constexpr int kGroup = 32;           // chunks per first-level fold group
+constexpr int kFoldBatch = 16;       // partial loads in flight per thread in the group fold
 constexpr double kPi = 3.141592653589793;
 constexpr double kTwoPi = 6.283185307179586;
 
@@ -440,19 +441,19 @@ __device__ __forceinline__ void hs_fold(const FoldArgs &a, int pat, int chunk, c
     if (!s_last) return;
     __threadfence();
     double2 *gp = a.gpart + (int64_t)pat * a.gpart_stride;
-    // Loads are issued 8 at a time ahead of the (chunk-ordered) sums: a few L2
+    // Loads are issued kFoldBatch at a time ahead of the (chunk-ordered) sums: a few L2
     // round trips on the fold tail instead of c1 - c0 dependent ones.
     if (a.partials64) {
         const double2 *part = a.partials64 + (int64_t)pat * a.part_stride;
         for (int k = tid; k < np; k += kThreads) {
             double sx = 0.0, sy = 0.0;
-            for (int cb = c0; cb < c1; cb += 8) {
-                double2 v[8];
+            for (int cb = c0; cb < c1; cb += kFoldBatch) {
+                double2 v[kFoldBatch];
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
+                for (int c = 0; c < kFoldBatch; ++c)
                     if (cb + c < c1) v[c] = __ldcg(part + (int64_t)(cb + c) * np + k);
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
+                for (int c = 0; c < kFoldBatch; ++c)
                     if (cb + c < c1) {
                         sx += v[c].x;
                         sy += v[c].y;
@@ -464,13 +465,13 @@ __device__ __forceinline__ void hs_fold(const FoldArgs &a, int pat, int chunk, c
         const float2 *part = a.partials + (int64_t)pat * a.part_stride;
         for (int k = tid; k < np; k += kThreads) {
             double sx = 0.0, sy = 0.0;
-            for (int cb = c0; cb < c1; cb += 8) {
-                float2 v[8];
+            for (int cb = c0; cb < c1; cb += kFoldBatch) {
+                float2 v[kFoldBatch];
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
+                for (int c = 0; c < kFoldBatch; ++c)
                     if (cb + c < c1) v[c] = __ldcg(part + (int64_t)(cb + c) * np + k);
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
+                for (int c = 0; c < kFoldBatch; ++c)
                     if (cb + c < c1) {
                         sx += (double)v[c].x;
                         sy += (double)v[c].y;
