@@ -96,9 +96,18 @@ constexpr int kUTmem = 256;      // TMEM columns per CTA (two CTAs per SM)
 #ifndef HS_UMMA_RING
 #define HS_UMMA_RING 3
 #endif
-constexpr int kUA = HS_UMMA_RING;  // A ring: gy planes (backward, TMA) / b' (forward, threads)
-constexpr int kUB = HS_UMMA_RING;  // B ring: X' (backward, threads) / X^T planes (forward, TMA)
-constexpr int kUD = kUA - 2;       // TMA prefetch distance (steps ahead of the MMA issue)
+// The spot-chunked variant (np > 112) runs one CTA per SM, whose shared
+// memory holds deeper rings: more k-steps of MMAs in flight (a k-step's
+// MMAs take ~2.6k cycles from issue to completion, four times their
+// tensor-pipe time, so two in flight leave the pipe idle).
+#ifndef HS_UMMA_RING_CH
+#define HS_UMMA_RING_CH 6
+#endif
+// ring depth (A ring: gy planes (backward, TMA) / b' (forward, threads);
+// B ring: X' (backward, threads) / X^T planes (forward, TMA))
+__host__ __device__ constexpr int hs_umma_ring(int np) { return np <= 112 ? HS_UMMA_RING : HS_UMMA_RING_CH; }
+constexpr int kUA = HS_UMMA_RING;  // ring of the np <= 112 variants
+constexpr int kUD = 1;             // TMA prefetch distance (steps ahead of the MMA issue)
 constexpr int kUMinBlocks = kUA <= 3 ? 2 : 1;  // CTAs per SM the shared memory allows
 constexpr int kUAPl = kUR * 32;                     // A plane [128 rows][32 bytes of K] (4 KB)
 constexpr int kUASlot = 4 * kUAPl;                  // 16 KB
@@ -109,7 +118,7 @@ __host__ __device__ constexpr int hs_umma_bslot(int) { return 4 * 2 * kUC * 32; 
 __host__ __device__ constexpr size_t hs_umma_smem_bytes(int np)
 {
     // rings + 128 B alignment slack + E reduce scratch [4 groups][8 warps][32] float + coef [np]
-    return (size_t)kUA * kUASlot + (size_t)kUB * hs_umma_bslot(np <= kUNPMax ? np : kUNPC) + 128 +
+    return (size_t)hs_umma_ring(np) * (kUASlot + hs_umma_bslot(np <= kUNPMax ? np : kUNPC)) + 128 +
            4 * 8 * 32 * sizeof(float) + 8 * (size_t)np;
 }
 
@@ -396,10 +405,12 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     constexpr uint32_t FLBO = (NP / 8) * 128;
     constexpr int KH = NP / 2;               // spots per thread in the E epilogue
     constexpr int kUBSlot = hs_umma_bslot(NP);
+    constexpr int RA = hs_umma_ring(NP), RB = RA;  // ring slots
+    constexpr int RW = RA - kUD;  // MMA wait distance: step j reuses the slots of step j - RW
     extern __shared__ __align__(128) unsigned char smu[];
     // MMA done [0, 4), A full (gy TMA) [4, 8), B full (X^T TMA) [8, 11),
     // operands written (all threads arrive) [11, 15)
-    __shared__ __align__(8) unsigned long long mbar[3 * kUA + kUB];
+    __shared__ __align__(8) unsigned long long mbar[3 * RA + RB];
     __shared__ uint32_t s_tmem;
 
     hs_pdl_launch_next();
@@ -429,8 +440,8 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
 
     unsigned char *sbase = reinterpret_cast<unsigned char *>(((uintptr_t)smu + 127) & ~(uintptr_t)127);
     const uint32_t sb = hs_smem_addr(sbase);
-    const uint32_t sa = sb, sbb = sb + kUA * kUASlot;  // A ring, B ring
-    float *red = reinterpret_cast<float *>(sbase + kUA * kUASlot + kUB * kUBSlot);  // [4][8][32]
+    const uint32_t sa = sb, sbb = sb + RA * kUASlot;  // A ring, B ring
+    float *red = reinterpret_cast<float *>(sbase + RA * kUASlot + RB * kUBSlot);  // [4][8][32]
     float2 *coef_s = reinterpret_cast<float2 *>(red + 4 * 8 * 32);                  // [np]
     const int grow = r0 + row;
     const bool row_in = grow < a.side;
@@ -466,7 +477,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     const uint32_t bar = hs_smem_addr(&mbar[0]);
-    const uint32_t bar_af = bar + 8 * kUA, bar_bf = bar + 16 * kUA, bar_op = bar + 8 * (2 * kUA + kUB);
+    const uint32_t bar_op = bar + 8 * (2 * RA + RB);
     auto bulk = [](uint32_t dst, const float *src, uint32_t bytes, uint32_t fb) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -474,24 +485,25 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
                      "l"(src), "r"(bytes), "r"(fb)
                      : "memory");
     };
-    // (thread 0) gy planes of backward step j -> A slot j % 4, two steps
-    // ahead (slot last used by j - 4); X^T planes of forward step j -> B slot
-    // j % 3, one step ahead (slot last used by j - 3).  Issued at step i after
-    // the wait for MMA(i - 2).
+    // (warp 1) gy planes of backward step j -> A slot j % RA, X^T planes of
+    // forward step j -> B slot j % RB, kUD steps ahead, issued at step i after
+    // the wait for MMA(i - RW).  The copy is one more arrival (with its byte
+    // count) on step j's operand barrier, so thread 0 waits once per step for
+    // the threads' operands and the TMA together.
     auto tma_ahead = [&](int i) {
         const int j = i + kUD;
         if (j < ksteps) {
-            bulk(sa + (j % kUA) * kUASlot, gyp + (int64_t)j * (kUASlot / 4), kUASlot, bar_af + 8 * (j % kUA));
+            bulk(sa + (j % RA) * kUASlot, gyp + (int64_t)j * (kUASlot / 4), kUASlot, bar_op + 8 * (j % RA));
         } else if (j < nsteps) {
             const int f = j - ksteps;  // spot chunk f / 8, column block f % 8
-            bulk(sbb + (j % kUB) * kUBSlot, xtp + ((int64_t)(f % NCC) * nsc + f / NCC) * FPL, 4 * FPL,
-                 bar_bf + 8 * (j % kUB));
+            bulk(sbb + (j % RB) * kUBSlot, xtp + ((int64_t)(f % NCC) * nsc + f / NCC) * FPL, 4 * FPL,
+                 bar_op + 8 * (j % RA));
         }
     };
     if (tid == 0) {
-        for (int i = 0; i < 2 * kUA + kUB; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar + 8 * i));
-        for (int i = 0; i < kUA; ++i)  // one (elected) arrival per warp
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_op + 8 * i), "n"(kUThreads / 32));
+        for (int i = 0; i < 2 * RA + RB; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar + 8 * i));
+        for (int i = 0; i < RA; ++i)  // one (elected) arrival per warp + the step's TMA
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_op + 8 * i), "n"(kUThreads / 32 + 1));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = -kUD; i < 0; ++i) tma_ahead(i);  // steps 0 .. kUD-1
     }
@@ -506,25 +518,12 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     // happen in order, never two phases behind.
     int done = 0;  // steps known complete
     auto wait_mma = [&](int j) {
-        for (; done <= j; ++done) hs_mbar_wait(bar + 8 * (done % kUA), (uint32_t)(done / kUA) & 1u);
+        for (; done <= j; ++done) hs_mbar_wait(bar + 8 * (done % RA), (uint32_t)(done / RA) & 1u);
         hs_tc_fence_after();
-    };
-    // TMA completions (thread 0 only): in step order per slot
-    uint32_t af_ph = 0, bf_ph = 0;  // parity bit per slot
-    auto wait_tma = [&](int j) {
-        if (j < ksteps) {
-            const int s = j % kUA;
-            hs_mbar_wait(bar_af + 8 * s, (af_ph >> s) & 1u);
-            af_ph ^= 1u << s;
-        } else {
-            const int s = j % kUB;
-            hs_mbar_wait(bar_bf + 8 * s, (bf_ph >> s) & 1u);
-            bf_ph ^= 1u << s;
-        }
     };
     auto commit = [&](int j) {  // thread 0, after issuing step j's MMAs
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         bar + 8 * (j % kUA))
+                         bar + 8 * (j % RA))
                      : "memory");
     };
     // Step j's operands written by the threads (generic proxy; TMEM reads
@@ -535,14 +534,25 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     // Each thread fences its own writes into the async proxy; the warp
     // converges and one lane arrives for it (256 single-thread arrivals on
     // one barrier word serialised into ~1k cycles per step).
-    auto publish = [&](int j) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        hs_tc_fence_before();
-        __syncwarp();
-        if (lane == 0)
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_op + 8 * (j % kUA)) : "memory");
+    // Backward steps (bwd): warp 0 -- the issuing thread's own warp, which
+    // writes no operand -- does not arrive; warp 1 arrives for it (count 2).
+    // At a fold step of the spot-chunked variant warp 0's TMEM reads are
+    // ordered before thread 0's MMAs by the tcgen05 fence and the warp sync.
+    auto publish = [&](int j, bool bwd = false, bool fold_step = false) {
+        if (!(bwd && warp == 0)) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            hs_tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar_op + 8 * (j % RA)),
+                             "r"((bwd && warp == 1) ? 2u : 1u)
+                             : "memory");
+        } else if (fold_step) {
+            hs_tc_fence_before();
+            __syncwarp();
+        }
         if (tid == 0) {
-            hs_mbar_wait(bar_op + 8 * (j % kUA), (uint32_t)(j / kUA) & 1u);
+            hs_mbar_wait(bar_op + 8 * (j % RA), (uint32_t)(j / RA) & 1u);
             hs_tc_fence_after();
             if (j < 16) TR(0, 96 + j);
         }
@@ -551,7 +561,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     // step j's MMAs (thread 0): A slot j % 4 (LBO 2048, SBO 128), B slot j % 3
     auto issue = [&](int j, uint32_t dr, uint32_t di, uint32_t lbo, uint32_t bpl, uint32_t id, uint32_t idn,
                      uint32_t acc) {
-        const uint32_t as = sa + (j % kUA) * kUASlot, bs = sbb + (j % kUB) * kUBSlot;
+        const uint32_t as = sa + (j % RA) * kUASlot, bs = sbb + (j % RB) * kUBSlot;
         const uint64_t xb[4] = {hs_sdesc(bs, lbo, 128), hs_sdesc(bs + bpl, lbo, 128), hs_sdesc(bs + 2 * bpl, lbo, 128),
                                 hs_sdesc(bs + 3 * bpl, lbo, 128)};
         hs_cmma(mma_ss, dr, di, [&](int pl) { return hs_sdesc(as + pl * kUAPl, 2048, 128); }, xb, id, idn, acc);
@@ -561,7 +571,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     // with B planes {B1_h, B1_l, B2_h, B2_l} of 128 rows: 6 MMAs, no negation
     const uint32_t idb = hs_idesc_tf32(2 * kUC, false);
     auto issue_bwd = [&](int j, uint32_t d, uint32_t acc) {
-        const uint32_t as = sa + (j % kUA) * kUASlot, bs = sbb + (j % kUB) * kUBSlot;
+        const uint32_t as = sa + (j % RA) * kUASlot, bs = sbb + (j % RB) * kUBSlot;
         auto A = [&](int pl) { return hs_sdesc(as + pl * kUAPl, 2048, 128); };
         auto B = [&](int pl) { return hs_sdesc(bs + pl * kUAPl, 2048, 128); };
         hs_mma_ss(d, A(0), B(0), idb, acc);
@@ -625,16 +635,17 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
         load_b(1, xn);
     }
     for (int ks = 0; ks < ksteps; ++ks) {
-        if (ks >= 2) wait_mma(ks - 2);  // A slot of ks + 1, B slot of ks free
+        if (ks >= RW) wait_mma(ks - RW);  // A slot of ks + kUD, B slot of ks free
+        const bool fold_step = CH && folded < (ks - RW + 1) / KG;  // uniform
         if (ks < 16) TR(kUThreads - 2 * kUC, 64 + ks);
         if (ks < 16) TR(0, 32 + ks);
-        if (CH)  // groups whose last step is <= ks - 2 (group g is read before group g + 2 reuses its region)
-            while (folded < (ks - 1) / KG) fold_group();
-        if (tid == 0) tma_ahead(ks);
+        if (CH)  // groups whose last step is <= ks - RW (group g is read before group g + 2 reuses its region)
+            while (folded < (ks - RW + 1) / KG) fold_group();
+        if (tid == 32) tma_ahead(ks);  // warp 1 issues the TMAs, beside thread 0's MMA issue
         if (ks < 16) TR(0, 48 + ks);
         if (xb_on) {  // step ks's X' chunks (built ahead), one 16-byte chunk per plane
             // planes [128 rows][kUF spots] (hs_uoffb): B1 = [Xr; Xi], B2 = [-Xi; Xr]
-            unsigned char *d = sbase + kUA * kUASlot + (ks % kUB) * kUBSlot + xb_c * 16 + xb_kq * 2048;
+            unsigned char *d = sbase + RA * kUASlot + (ks % RB) * kUBSlot + xb_c * 16 + xb_kq * 2048;
             constexpr int R64 = kUC * 16;  // row 64
             *reinterpret_cast<uint4 *>(d) = pre[0];
             *reinterpret_cast<uint4 *>(d + R64) = pre[2];
@@ -647,14 +658,12 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
         }
         if (ks < 16) TR(kUThreads - 2 * kUC, 80 + ks);
 
-        publish(ks);
+        publish(ks, true, fold_step);
         if (xb_on && ks + 1 < ksteps) {
             make_x(ks + 1);
             load_b(ks + 2, xn);
         }
         if (tid == 0) {
-            wait_tma(ks);  // gy planes landed
-            if (ks < 16) TR(0, 112 + ks);
             const uint32_t dr = CH ? tm + (uint32_t)(((ks / KG) & 1) * 128) : tm;
             issue_bwd(ks, dr, (CH ? ks % KG : ks) ? 1u : 0u);
             if (ks < 16) TR(0, 2 + ks);
@@ -759,8 +768,8 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
 #pragma unroll
     for (int cc = 0; cc < NCC; ++cc) {
         const int j = ksteps + sc * NCC + cc;  // step
-        wait_mma(j - 2);             // A slot of j (last used by j - 3), B slot of j + 1 (j - 2) free
-        if (tid == 0) tma_ahead(j);
+        wait_mma(j - RW);            // A slot of j (last used by j - RA), B slot of j + kUD free
+        if (tid == 32) tma_ahead(j);
         if constexpr (kF16) {  // b' (this thread's row): columns 4h .. 4h+3 of both 8-column K halves
 #pragma unroll
             for (int qh = 0; qh < 2; ++qh) {
@@ -771,7 +780,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
                     hs_split1(br[4 * g + jj], hb[jj], lb[jj]);
                     hs_split1(bi[4 * g + jj], hb[4 + jj], lb[4 + jj]);
                 }
-                unsigned char *d = sbase + (j % kUA) * kUASlot + row * 16 + qh * 2048 + h * 8;
+                unsigned char *d = sbase + (j % RA) * kUASlot + row * 16 + qh * 2048 + h * 8;
                 *reinterpret_cast<uint2 *>(d) = make_uint2(hb[0] | hb[1] << 16, hb[2] | hb[3] << 16);
                 *reinterpret_cast<uint2 *>(d + kUAPl) = make_uint2(lb[0] | lb[1] << 16, lb[2] | lb[3] << 16);
                 *reinterpret_cast<uint2 *>(d + 2 * kUAPl) = make_uint2(hb[4] | hb[5] << 16, hb[6] | hb[7] << 16);
@@ -781,7 +790,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
             uint4 rh, rl, ih, il;
             hs_split_chunk(&br[4 * cc], rh, rl);
             hs_split_chunk(&bi[4 * cc], ih, il);
-            unsigned char *d = sbase + (j % kUA) * kUASlot + row * 16 + h * 2048;
+            unsigned char *d = sbase + (j % RA) * kUASlot + row * 16 + h * 2048;
             *reinterpret_cast<uint4 *>(d) = rh;
             *reinterpret_cast<uint4 *>(d + kUAPl) = rl;
             *reinterpret_cast<uint4 *>(d + 2 * kUAPl) = ih;
@@ -789,7 +798,6 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
         }
         publish(j);  // (cc = 0: also orders the S / previous chunk's T reads before T is overwritten)
         if (tid == 0) {
-            wait_tma(j);  // X^T planes landed
             issue(j, tm, tm + NP, FLBO, FPL, idf, idfn, cc ? 1u : 0u);
             if (sc == 0) TR(0, 20 + cc);
         }
