@@ -304,16 +304,19 @@ __device__ __forceinline__ void hs_mma_ts(uint32_t d, uint32_t a, uint64_t b, ui
                      "r"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
-// A from shared memory
+// A from shared memory.  Called by a whole converged warp with warp-uniform
+// operands; one elected lane issues (the operands stay in uniform
+// registers -- issued from a one-thread branch, every MMA was wrapped in an
+// ELECT / R2UR / BRA.U.ANY loop, ~100 cycles each).
 __device__ __forceinline__ void hs_mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc)
 {
     if constexpr (kF16)
-        asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                     " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        asm volatile("{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+                     " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
                      "l"(a), "l"(b), "r"(idesc), "r"(acc));
     else
-        asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                     " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        asm volatile("{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+                     " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
                      "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
@@ -522,7 +525,8 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
         hs_tc_fence_after();
     };
     auto commit = [&](int j) {  // thread 0, after issuing step j's MMAs
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+        asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+                     " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
                          bar + 8 * (j % RA))
                      : "memory");
     };
@@ -551,7 +555,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
             hs_tc_fence_before();
             __syncwarp();
         }
-        if (tid == 0) {
+        if (warp == 0) {  // the issuing warp, converged
             hs_mbar_wait(bar_op + 8 * (j % RA), (uint32_t)(j / RA) & 1u);
             hs_tc_fence_after();
             if (j < 16) TR(0, 96 + j);
@@ -663,7 +667,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
             make_x(ks + 1);
             load_b(ks + 2, xn);
         }
-        if (tid == 0) {
+        if (warp == 0) {
             const uint32_t dr = CH ? tm + (uint32_t)(((ks / KG) & 1) * 128) : tm;
             issue_bwd(ks, dr, (CH ? ks % KG : ks) ? 1u : 0u);
             if (ks < 16) TR(0, 2 + ks);
@@ -797,7 +801,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
             *reinterpret_cast<uint4 *>(d + 3 * kUAPl) = il;
         }
         publish(j);  // (cc = 0: also orders the S / previous chunk's T reads before T is overwritten)
-        if (tid == 0) {
+        if (warp == 0) {
             issue(j, tm, tm + NP, FLBO, FPL, idf, idfn, cc ? 1u : 0u);
             if (sc == 0) TR(0, 20 + cc);
         }
