@@ -28,37 +28,37 @@
 // one CTA per SM, the backward's k-steps summed in groups in registers.)
 // S is read once into registers (b: 32 columns per thread), which frees the
 // columns T reuses.  The operands that do not change between passes are
-// written once per table build by hs_umma_prep_kernel as tf32 hi/lo planes
+// written once per table build by hs_umma_prep_kernel as hi/lo planes (fp16)
 // already in the shared-memory operand layout -- gy (A of the backward,
 // [band][k-step] blocks of 16 KB) and X^T (B of the forward, 8-column blocks
 // of <= 16 KB) -- and each k-step's block is one TMA bulk copy, issued one
 // step ahead; the per-pass coefficients go on the B side of the backward
 // (X' = coef_k gx[c][k], built by warps 4-7) and b' (A of the forward) is
-// written by every thread for its row.  The gy planes also give the E
-// epilogue reads gy in fp32 from a row-coalesced copy written beside them.  Shared memory: A and
-// B rings of 3 x 16 KB, SWIZZLE_NONE K-major canonical layout (8 x 16-byte
-// core matrices).  Per k-step every thread arrives on an operand mbarrier
-// after writing its part (no CTA-wide barrier); thread 0 waits for it and
-// for the TMA, issues the MMAs and commits them to the step's MMA-done
-// barrier; the threads wait for the MMAs two steps back before reusing a slot.
+// written by every thread for its row.  The E epilogue reads gy in fp32
+// from a row-coalesced copy written beside the planes.  Shared memory: A and
+// B rings (3 slots of 16 KB at two CTAs per SM; 6 for the spot-chunked
+// variant at one CTA per SM), SWIZZLE_NONE K-major canonical layout (8 x
+// 16-byte core matrices).
 //
-// What bounds it (ncu, B = 16, profiles/round1/umma_full_pass.md): the
-// tensor pipe is ~39% active and its shared-memory operand reads ~32% (8 KB
-// per backward MMA, 7.5 KB per forward MMA); the per-tile CUDA-core work (b,
-// E reduce, fold) and the mbarrier waits make up the rest.
+// Roles per k-step j: the threads that write operands (warps 4-7 in the
+// backward, all warps in the forward) fence them into the async proxy and
+// arrive, one elected lane per warp, on operand barrier j % R; warp 1's
+// lane 0 issues the TMA of step j + 1 as one more arrival on that barrier
+// (expect_tx) after MMA(j + 1 - R) has freed the slot; the converged warp 0
+// waits once for the barrier and issues the step's MMAs and commit with
+// elect.sync (from a one-thread branch the compiler wrapped every MMA in an
+// ELECT / R2UR / BRA.U.ANY loop, ~100 cycles each).  Slots are reused R - 1
+// steps later, so up to R - 1 steps of MMAs are in flight.
 //
 // Per-CTA timeline (HS_UMMA_TRACE=1 with hs_time_kernel: clock64 at fixed
-// points of one CTA, B = 32, round 2): prologue 2.0k cycles, 14 backward
-// k-steps 1.6-1.7k cycles each (the 6 MMAs need ~400), b 5k, 8 forward
-// k-steps ~1.7k each, E epilogue ~13k, fold ~3.5k: ~66k per tile per CTA.
-// The k-step cadence is the shared-memory data path: a kind::tf32 MMA with
-// K = 8 reads 4 KB of A and 4 KB of B per 64 MMA cycles -- 128 B/cycle, the
-// whole smem bandwidth -- and the TMA (16 KB), the operand stores (16 KB)
-// and the other CTA's MMAs share it.  Deeper rings (1 CTA per SM, TMA 3-4
-// steps ahead: HS_UMMA_RING=4..6), one elected arrival per warp and moving
-// the issuer's wait behind its issue left the cadence unchanged; fewer smem
-// bytes per MAC (kind::f16 with a 2-term fp16 split, A from TMEM) is what
-// would move it.
+// points of one CTA; round 2 final).  B = 32, np = 112, two CTAs per SM:
+// prologue 2.6k cycles, 7 backward k-steps ~2k each, b 8.4k, 4 forward
+// k-steps ~1.7k, E epilogue 12.2k, fold 3.8k (52k per tile, two tiles
+// overlapping per SM).  Config 4 (np = 1008, one CTA per SM): 63 backward
+// k-steps ~1.5k each (was 2.1k before the issue changes above), then 8
+// forward spot chunks.  Tensor pipe ~25-28% active (ncu): the cadence is
+// the issue chain (barrier wait, descriptor moves to uniform registers,
+// 6-12 MMA issues, commit) and, per tile, the CUDA-core phases (b, E).
 //
 // Encodings (instruction descriptor, shared-memory descriptor, TMEM
 // st / ld, a_negate) are checked by tools/umma_probe.cu.
