@@ -51,6 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(ROOT, "build", "obj")
     os.makedirs(objdir, exist_ok=True)
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    if os.environ.get("HS_PROBES"):  # timing probes of the pass kernels (HS_SLAB_TRACE / HS_UMMA_TRACE)
+        compile_flags.append("-DHS_PROBES=1")
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")

@@ -40,6 +40,14 @@ namespace hs {
 constexpr int kThreads = 256;        // pass-kernel CTA size (8 warps)
 constexpr int kWarps = kThreads / 32;
 constexpr int kTargetChunks = 296;   // sparse lists: chunks per pattern (2 x 148 SMs)
+// Timing probes inside the pass kernels (HS_SLAB_TRACE / HS_UMMA_TRACE with
+// hs_time_kernel) are compiled in only with -DHS_PROBES=1 (build.py: HS_PROBES=1
+// in the environment); compiled out they cost nothing (2-3% of the tcgen05
+// pass when present).
+#ifndef HS_PROBES
+#define HS_PROBES 0
+#endif
+
 constexpr int kGroup = 32;           // chunks per first-level fold group
 constexpr int kFoldBatch = 16;       // partial loads in flight per thread in the group fold
 constexpr double kPi = 3.141592653589793;
@@ -282,6 +290,47 @@ static __global__ void hs_seed_kernel(int n, int np, const double *amp, const do
 }
 
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ float hs_rsqrt(float x)
+{
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// b = A conj(S)/|S| with arg(0) = 0 (kernels.py:136-137, solvers.py:96-101)
+__device__ __forceinline__ void hs_bvec(float sr, float si, float A, float &br, float &bi)
+{
+    const float m2 = fmaf(sr, sr, si * si);
+    if (__float_as_uint(m2) - 0x0d800000u < 0x64000000u) {  // 2^-100 <= m2 < 2^100
+        const float inv = A * hs_rsqrt(m2);
+        br = sr * inv;
+        bi = -si * inv;
+    } else if (sr != 0.f || si != 0.f) {
+        const float mx = fmaxf(fabsf(sr), fabsf(si));
+        const float xr = sr / mx, xi = si / mx;
+        const float inv = A * hs_rsqrt(fmaf(xr, xr, xi * xi));
+        br = xr * inv;
+        bi = -xi * inv;
+    } else {
+        br = A;
+        bi = 0.f;
+    }
+}
+
+// hs_bvec without branches: S is scaled by the power of two 2^-e that
+// brings max(|Sr|, |Si|) into [1, 2) before |S|^2 is formed.  Scaling by a
+// power of two is exact, so wherever hs_bvec takes its fast path the result
+// is bitwise the same; tiny and huge |S| need no separate path.
+__device__ __forceinline__ void hs_bvec_nb(float sr, float si, float A, float &br, float &bi)
+{
+    const float mx = fmaxf(fabsf(sr), fabsf(si));
+    const float sc = __int_as_float(0x7f000000 - (__float_as_int(mx) & 0x7f800000));  // 2^-e (2^127 for denormals)
+    const float xr = sr * sc, xi = si * sc;
+    const float inv = A * hs_rsqrt(fmaf(xr, xr, xi * xi));
+    br = mx > 0.f ? xr * inv : A;
+    bi = mx > 0.f ? -xi * inv : 0.f;
+}
+
 // Fixed-shape block reductions over kThreads values: a butterfly inside each
 // warp (every lane ends with the same bits: the pairs are commutative), then
 // the kWarps warp results combined in warp order.  Deterministic and ~4x

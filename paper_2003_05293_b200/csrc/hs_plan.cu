@@ -2383,7 +2383,7 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
         CUDA_TRY(cudaStreamSynchronize(p->stream));
         unsigned long long t[128];
         CUDA_TRY(cudaMemcpy(t, p->d_trace, sizeof t, cudaMemcpyDeviceToHost));
-        fprintf(stderr, "slab trace (cycles from CTA start):");
+        fprintf(stderr, "slab trace (cycles from CTA start%s):", HS_PROBES ? "" : "; empty: build with HS_PROBES=1");
         for (int i = 1; i < 128; ++i)
             if (t[i]) fprintf(stderr, " %d:%lld", i, (long long)(t[i] - t[0]));
         fprintf(stderr, "\n");
@@ -2396,7 +2396,7 @@ int hs_time_kernel(hs_plan *p, int which, int64_t subset, int reps, double *ms_p
         CUDA_TRY(cudaStreamSynchronize(p->stream));
         unsigned long long t[128];
         CUDA_TRY(cudaMemcpy(t, p->d_trace, sizeof t, cudaMemcpyDeviceToHost));
-        fprintf(stderr, "umma trace (cycles from CTA start):");
+        fprintf(stderr, "umma trace (cycles from CTA start%s):", HS_PROBES ? "" : "; empty: build with HS_PROBES=1");
         for (int i = 1; i < 128; ++i)
             if (t[i]) fprintf(stderr, " %d:%lld", i, (long long)(t[i] - t[0]));
         fprintf(stderr, "\n");

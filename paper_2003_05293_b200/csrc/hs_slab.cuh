@@ -88,47 +88,6 @@ __host__ __device__ constexpr size_t hs_slab_smem_bytes(int np, int sw)
     return sizeof(float2) * (size_t)np * sw + hs_slab_fixed_bytes(np);
 }
 
-__device__ __forceinline__ float hs_rsqrt(float x)
-{
-    float y;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-// b = A conj(S)/|S| with arg(0) = 0 (kernels.py:136-137, solvers.py:96-101)
-__device__ __forceinline__ void hs_bvec(float sr, float si, float A, float &br, float &bi)
-{
-    const float m2 = fmaf(sr, sr, si * si);
-    if (__float_as_uint(m2) - 0x0d800000u < 0x64000000u) {  // 2^-100 <= m2 < 2^100
-        const float inv = A * hs_rsqrt(m2);
-        br = sr * inv;
-        bi = -si * inv;
-    } else if (sr != 0.f || si != 0.f) {
-        const float mx = fmaxf(fabsf(sr), fabsf(si));
-        const float xr = sr / mx, xi = si / mx;
-        const float inv = A * hs_rsqrt(fmaf(xr, xr, xi * xi));
-        br = xr * inv;
-        bi = -xi * inv;
-    } else {
-        br = A;
-        bi = 0.f;
-    }
-}
-
-// hs_bvec without branches: S is scaled by the power of two 2^-e that
-// brings max(|Sr|, |Si|) into [1, 2) before |S|^2 is formed.  Scaling by a
-// power of two is exact, so wherever hs_bvec takes its fast path the result
-// is bitwise the same; tiny and huge |S| need no separate path.
-__device__ __forceinline__ void hs_bvec_nb(float sr, float si, float A, float &br, float &bi)
-{
-    const float mx = fmaxf(fabsf(sr), fabsf(si));
-    const float sc = __int_as_float(0x7f000000 - (__float_as_int(mx) & 0x7f800000));  // 2^-e (2^127 for denormals)
-    const float xr = sr * sc, xi = si * sc;
-    const float inv = A * hs_rsqrt(fmaf(xr, xr, xi * xi));
-    br = mx > 0.f ? xr * inv : A;
-    bi = mx > 0.f ? -xi * inv : 0.f;
-}
-
 __device__ __forceinline__ float2 hs_lds2(uint32_t addr)
 {
     float2 v;
@@ -160,7 +119,11 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
     hs_pdl_launch_next();
     const bool trc = a.trace && blockIdx.x == (gridDim.x > 20 ? 20u : gridDim.x / 2) && blockIdx.y == 0;
     auto TR = [&](int slot) {
+#if HS_PROBES
         if (trc && threadIdx.x == 0) a.trace[slot] = clock64();
+#else
+        (void)trc, (void)slot;
+#endif
     };
     TR(0);
     const int pat = blockIdx.y;

@@ -422,7 +422,11 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     // timing probe: clock64 at fixed points of one CTA (tile 100, pattern 0)
     const bool trc = a.trace && blockIdx.x == 100 && blockIdx.y == 0;
     auto TR = [&](int who, int slot) {
+#if HS_PROBES
         if (trc && (int)threadIdx.x == who) a.trace[slot] = clock64();
+#else
+        (void)trc, (void)who, (void)slot;
+#endif
     };
     TR(0, 0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -742,7 +746,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
         for (int jj = 0; jj < 8; ++jj) {
             const int i = 4 * cc + jj;
             const float A = br[i];
-            hs_bvec_exact(sr[jj], si[jj], A, br[i], bi[i]);
+            hs_bvec_nb(sr[jj], si[jj], A, br[i], bi[i]);  // branch-free: the 8 pixels interleave
             if (WRITE) {
                 const int c = c0 + (i / 4) * 8 + 4 * h + (i % 4);
                 if (row_in && c < a.side) {
