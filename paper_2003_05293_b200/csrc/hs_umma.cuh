@@ -177,6 +177,15 @@ __device__ __forceinline__ void hs_split1(float v, uint32_t &hb, uint32_t &lb)
     }
 }
 
+// fp16 hi/lo split of two values into packed words (v0 in the low half):
+// one paired conversion each way, bitwise the same as two hs_split1
+__device__ __forceinline__ void hs_split2(float v0, float v1, uint32_t &h, uint32_t &l)
+{
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(v1), "f"(v0));  // d.hi = cvt(a), d.lo = cvt(b)
+    const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&h));
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(v1 - f.y), "f"(v0 - f.x));
+}
+
 __device__ __forceinline__ void hs_put(unsigned char *p, uint32_t bits)
 {
     if constexpr (kF16) *reinterpret_cast<unsigned short *>(p) = (unsigned short)bits;
@@ -194,13 +203,16 @@ __device__ __forceinline__ void hs_split_store(float v, unsigned char *dst, int 
 // hi/lo split of one 16-byte core-matrix row chunk (kUQ values), and its negation
 __device__ __forceinline__ void hs_split_chunk(const float *v, uint4 &hi, uint4 &lo)
 {
-    uint32_t hb[kUQ], lb[kUQ];
-#pragma unroll
-    for (int i = 0; i < kUQ; ++i) hs_split1(v[i], hb[i], lb[i]);
     if constexpr (kF16) {
-        hi = make_uint4(hb[0] | hb[1] << 16, hb[2] | hb[3] << 16, hb[4] | hb[5] << 16, hb[6] | hb[7] << 16);
-        lo = make_uint4(lb[0] | lb[1] << 16, lb[2] | lb[3] << 16, lb[4] | lb[5] << 16, lb[6] | lb[7] << 16);
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hs_split2(v[2 * i], v[2 * i + 1], hw[i], lw[i]);
+        hi = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        lo = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     } else {
+        uint32_t hb[kUQ], lb[kUQ];
+#pragma unroll
+        for (int i = 0; i < kUQ; ++i) hs_split1(v[i], hb[i], lb[i]);
         hi = make_uint4(hb[0], hb[1], hb[2], hb[3]);
         lo = make_uint4(lb[0], lb[1], lb[2], lb[3]);
     }
@@ -782,17 +794,17 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
 #pragma unroll
             for (int qh = 0; qh < 2; ++qh) {
                 const int g = 2 * cc + qh;  // 8-column group of the row
-                uint32_t hb[8], lb[8];
+                uint32_t rh[2], rl[2], ih[2], il[2];
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                    hs_split1(br[4 * g + jj], hb[jj], lb[jj]);
-                    hs_split1(bi[4 * g + jj], hb[4 + jj], lb[4 + jj]);
+                for (int jj = 0; jj < 2; ++jj) {
+                    hs_split2(br[4 * g + 2 * jj], br[4 * g + 2 * jj + 1], rh[jj], rl[jj]);
+                    hs_split2(bi[4 * g + 2 * jj], bi[4 * g + 2 * jj + 1], ih[jj], il[jj]);
                 }
                 unsigned char *d = sbase + (j % RA) * kUASlot + row * 16 + qh * 2048 + h * 8;
-                *reinterpret_cast<uint2 *>(d) = make_uint2(hb[0] | hb[1] << 16, hb[2] | hb[3] << 16);
-                *reinterpret_cast<uint2 *>(d + kUAPl) = make_uint2(lb[0] | lb[1] << 16, lb[2] | lb[3] << 16);
-                *reinterpret_cast<uint2 *>(d + 2 * kUAPl) = make_uint2(hb[4] | hb[5] << 16, hb[6] | hb[7] << 16);
-                *reinterpret_cast<uint2 *>(d + 3 * kUAPl) = make_uint2(lb[4] | lb[5] << 16, lb[6] | lb[7] << 16);
+                *reinterpret_cast<uint2 *>(d) = make_uint2(rh[0], rh[1]);
+                *reinterpret_cast<uint2 *>(d + kUAPl) = make_uint2(rl[0], rl[1]);
+                *reinterpret_cast<uint2 *>(d + 2 * kUAPl) = make_uint2(ih[0], ih[1]);
+                *reinterpret_cast<uint2 *>(d + 3 * kUAPl) = make_uint2(il[0], il[1]);
             }
         } else {  // b' (this thread's row, columns 4h .. 4h+3 of the k-step = K half h)
             uint4 rh, rl, ih, il;
