@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     for (int k = tid; k < a.np; k += kUThreads) coef_s[k] = a.coef[(int64_t)pat * a.np + k];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(hs_smem_addr(&s_tmem)),
-                     "n"(kUTmem));
+                     "n"(NP == kUNPC ? 2 * kUTmem : kUTmem));  // spot-chunked: 512 (double-buffered T)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     const uint32_t bar = hs_smem_addr(&mbar[0]);
@@ -786,8 +786,12 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
     // [NP spots][kUF columns] ((k/8)*128 + (c/kUQ)*FLBO + (k%8)*16 + (c%kUQ)*kUEB), TMA
     const uint32_t idf = hs_idesc_tf32(NP, false), idfn = hs_idesc_tf32(NP, true);
     float2 *out = a.f.partials + (int64_t)pat * a.f.part_stride + (int64_t)tile * a.np;
-#pragma unroll 1
-    for (int sc = 0; sc < nsc; ++sc) {
+    // T of spot chunk sc lives in TMEM columns tb(sc): the spot-chunked
+    // variant (one CTA per SM, 512 columns) double-buffers it, so chunk
+    // sc + 1's MMAs run while chunk sc's E epilogue reads its T
+    constexpr bool TB = NP == kUNPC;
+    auto tb = [&](int sc) -> uint32_t { return TB ? (uint32_t)((sc & 1) * 256) : 0u; };
+    auto fwd_chunk = [&](int sc) {
 #pragma unroll
     for (int cc = 0; cc < NCC; ++cc) {
         const int j = ksteps + sc * NCC + cc;  // step
@@ -821,10 +825,16 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
         }
         publish(j);  // (cc = 0: also orders the S / previous chunk's T reads before T is overwritten)
         if (warp == 0) {
-            issue(j, tm, tm + NP, FLBO, FPL, idf, idfn, cc ? 1u : 0u);
+            issue(j, tm + tb(sc), tm + tb(sc) + NP, FLBO, FPL, idf, idfn, cc ? 1u : 0u);
             if (sc == 0) TR(0, 20 + cc);
         }
     }
+    };
+    if (TB) fwd_chunk(0);
+#pragma unroll 1
+    for (int sc = 0; sc < nsc; ++sc) {
+    if (!TB) fwd_chunk(sc);
+    else if (sc + 1 < nsc) fwd_chunk(sc + 1);  // after chunk sc - 1's E reads (program order + publish)
     wait_mma(ksteps + (sc + 1) * NCC - 1);
     if (sc == 0) TR(0, 28);
 
@@ -868,8 +878,8 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
 #pragma unroll
         for (int e = 0; e < 2; ++e)
             if (8 * e < KQ) {
-                hs_tc_ld8(tl + kk + 8 * e, *reinterpret_cast<float (*)[8]>(tq[e]));
-                hs_tc_ld8(tl + NP + kk + 8 * e, *reinterpret_cast<float (*)[8]>(tq[e] + 8));
+                hs_tc_ld8(tl + tb(sc) + kk + 8 * e, *reinterpret_cast<float (*)[8]>(tq[e]));
+                hs_tc_ld8(tl + tb(sc) + NP + kk + 8 * e, *reinterpret_cast<float (*)[8]>(tq[e] + 8));
             }
         hs_tc_wait_ld();
 #pragma unroll
@@ -924,7 +934,8 @@ __global__ void __launch_bounds__(kUThreads, NP == kUNPC ? 1 : kUMinBlocks) hs_u
 
     hs_tc_fence_before();
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(kUTmem));
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(NP == kUNPC ? 2 * kUTmem : kUTmem));
     if (a.f.u.act != ACT_NONE) hs_fold(a.f, pat, tile, reinterpret_cast<char *>(sbase));
     TR(0, 30);
 }
