@@ -114,7 +114,6 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
     static_assert(GPW * WPC == kSlabStreams, "32 streams per chunk");
     extern __shared__ float4 sm4[];
     __shared__ __align__(8) unsigned long long bar;
-    __shared__ int s_next_c0;
 
     hs_pdl_launch_next();
     const bool trc = a.trace && blockIdx.x == (gridDim.x > 20 ? 20u : gridDim.x / 2) && blockIdx.y == 0;
@@ -375,7 +374,7 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
     };
 
     // End of chunk qi: flush, sum the 32 streams in a fixed order, reset, stage.
-    auto chunk_end = [&](int qi) {
+    auto chunk_end = [&](int qi, int cs_next) {
         if (rcur >= 0) flush();
         rcur = -1;
         // the warp's GPW streams: symmetric butterfly adds, kept in stream
@@ -404,10 +403,15 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
                 }
             }
         }
-        __syncthreads();
+        // whole-chunk CTAs: each half-chunk's 8 warps sync on their own named
+        // barrier (1 + half), so one half's reduction does not wait for the
+        // other half's last trip
         constexpr int HALVES = HALF ? 1 : 2;
-        for (int idx = tid; idx < HALVES * NP; idx += NT) {
-            const int hh = HALF ? half : idx / NP, k = HALF ? idx : idx - hh * NP;
+        const int my_half = HALF ? half : gw / (WPC / 2);
+        if constexpr (HALF) __syncthreads();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + my_half), "n"(NT / 2) : "memory");
+        for (int idx = HALF ? tid : tid - my_half * (NT / 2); idx < NP; idx += HALF ? NT : NT / 2) {
+            const int hh = my_half, k = idx;
             float x = 0.f, y = 0.f;
 #pragma unroll
             for (int w = 0; w < WPC / 2; ++w) {
@@ -423,11 +427,13 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
         store_ent(qi + 2);  // chunk qi's buffer is consumed
         __syncwarp();
         if (qi + 1 < nq) {
-            const int cs = s_next_c0;  // read at the chunk's start
+            const int cs = cs_next;  // loaded at the chunk's start (a register: the halves do not sync here)
             if (cs != c0)
                 stage(cs);        // begins with __syncthreads
-            else
+            else if constexpr (HALF)
                 __syncthreads();  // Es reset visible before the next flushes
+            else
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + my_half), "n"(NT / 2) : "memory");
         }
     };
 
@@ -514,9 +520,8 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
     for (int qi = 0; qi < nq; ++qi) {
         if (qi < 16) TR(2 + 3 * qi);
         fetch_ent(qi + 2);
-        // the next chunk's slab origin, read now (the previous chunk's last
-        // barrier ordered the previous reads of s_next_c0 before this write)
-        if (tid == 0 && qi + 1 < nq) s_next_c0 = __ldg(a.chunk_c0 + q0 + qi + 1);
+        // the next chunk's slab origin, loaded now, used at the chunk's end
+        const int cs_next = (qi + 1 < nq) ? __ldg(a.chunk_c0 + q0 + qi + 1) : 0;
         if constexpr (PIPE) {
             pipe_chunk((qi & 1) ? ent1 : ent0);
         } else {
@@ -527,7 +532,7 @@ __global__ void __launch_bounds__(HALF ? 16 * G : 32 * G, 1) hs_slab_kernel(cons
             }
         }
         if (qi < 16) TR(3 + 3 * qi);
-        chunk_end(qi);
+        chunk_end(qi, cs_next);
         if (qi < 16) TR(4 + 3 * qi);
     }
     TR(60);
