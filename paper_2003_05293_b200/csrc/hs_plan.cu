@@ -229,7 +229,7 @@ struct hs_plan {
     cudaStream_t copy_stream = nullptr;     // D2H of phases, overlapped with solves
     cudaStream_t widen_stream[2] = {nullptr, nullptr};  // host widening of a slot's codes
     cudaEvent_t landed[2][kWidenChunksMax + 1] = {};     // a slot's code chunks (+ f64 part) reached the host
-    double e2e_f64_frac = 0.625;          // hs_solve_host: share of patterns shipped as f64 (HS_E2E_F64_FRAC)
+    double e2e_f64_frac = 0.375;          // hs_solve_host: share of patterns shipped as f64 (HS_E2E_F64_FRAC)
     cudaEvent_t solved[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
     double *d_trace_w = nullptr, *d_trace_m = nullptr;
     int64_t trace_cap = 0;
