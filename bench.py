@@ -313,9 +313,11 @@ def umma_roofline(pupil, batch, n, ms):
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense f16 = bf16 rate)"
             if bf16 else "B200_PROFILING.md nominal dense bf16/fp16 2.25 PFLOP/s",
-            "note": "shared-memory-operand MMAs cost ~118 cycles each at N <= 128 (tools/mma_rate.cu: "
-                    "twice the ideal); per-tile timeline in csrc/hs_umma.cuh (HS_UMMA_TRACE): the "
-                    "b and E epilogues run serially with the MMAs inside a CTA"}
+            "note": "executed f16 flops include the 2-term split (3 products per real product) and "
+                    "tile / spot padding; tensor pipe ~29% active by ncu: per tile the b and E "
+                    "epilogues (CUDA cores) run serially with the MMAs inside a CTA and overlap only "
+                    "across the SM's two CTAs (per-tile timeline: csrc/hs_umma.cuh, HS_PROBES=1 build "
+                    "with HS_UMMA_TRACE=1)"}
 
 
 def run_ours(args):
